@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py — one step of the hybridization hot path per iteration, timed on the device.
+
+A step (SURVEY.md §8(a) rows a1-a8 over one batch): hdg_condense (stage, LU with partial pivoting, local solves,
+Schur complement, factor store) -> hdg_assemble_skeleton (+ shared-face exchange and accumulate when N > 1)
+-> hdg_backsubstitute with a seeded trace vector lambda. The plan (row a0) is built once, outside the timed
+region, as in a Newton loop on a fixed mesh.
+
+Workload: BASELINE.json configs[3] ("C4", NS mixed HDG p=3, 131072 triangles, n_e=120, n_f=48) by default — the
+largest configuration that fits one B200 (C5 needs ~490 GB). Synthetic inputs from the seeded generator, created
+directly in HBM (bit-identical to the host generator the oracle uses). Inputs (~30 GB) exceed L2 (126 MB), so no
+L2 flush is needed between steps.
+
+Contract: python bench.py --gpus N --steps K --warmup W [--impl reference] ; torchrun for N > 1 (one rank per
+GPU, element slabs, NCCL for the shared-face exchange). Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "element condensations/s + back-subs/s (fp64), % of FP64/HBM roofline"
+
+
+def algorithmic(ne, nf):
+    """SURVEY.md §8(d) per-element work (one HBM pass; nothing the method avoids)."""
+    ne = np.asarray(ne, dtype=np.float64)
+    nf = np.asarray(nf, dtype=np.float64)
+    cf = ne * (ne - 1) * (4 * ne + 1) / 6 + (nf + 1) * (2 * ne * ne - ne) + 2 * nf * ne * (nf + 1)
+    cb = 8 * (ne * ne + 2 * ne * nf + nf * nf + ne + nf) + 8 * (nf * nf + nf) + (8 * ne * ne + 4 * ne)
+    bf = 2 * ne * nf + 2 * ne * ne
+    bb = 8 * (ne * ne + ne * nf + 2 * ne + nf) + 4 * ne
+    return dict(condense_flops=float(cf.sum()), condense_bytes=float(cb.sum()), backsub_flops=float(bf.sum()),
+                backsub_bytes=float(bb.sum()))
+
+
+def measured_peaks():
+    peaks = {}
+    try:
+        peaks.update(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))))
+    except Exception:
+        pass
+    return peaks
+
+
+def fp64_peak_in_run():
+    """K9: FP64 peak measured on this box in this run (tools/peaks: DMMA and DFMA loops)."""
+    exe = os.path.join(ROOT, "tools", "peaks")
+    try:
+        out = subprocess.run([exe, "fp64"], capture_output=True, text=True, timeout=120).stdout
+        d = json.loads(out.strip().splitlines()[-1])
+        dmma = max(v for k, v in d.items() if k.startswith("dmma"))
+        dfma = max(v for k, v in d.items() if k.startswith("dfma"))
+        return dmma, dfma
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"hdg_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                try:
+                    rows.append((float(f[1]), float(f[2]), f[5:9]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i in range(4) if r[i].lower() == "active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
+                "samples": len(rows), "reasons": reasons}
+
+
+def slab_bounds(E: int, n: int):
+    return np.array([(r * E) // n for r in range(n + 1)], dtype=np.int64)
+
+
+def oracle_sample(w, seconds: float, lam, max_elems=None):
+    """The oracle (as it stands) on a bounded sample of the workload: condense + assemble (rows owned by the
+    sample) + back-substitute for the first m elements. Returns (elements/s, m, wall seconds, threads)."""
+    import oracle
+    import gen
+
+    def run(m):
+        blk = gen.host_blocks(w, 0, m)
+        t0 = time.perf_counter()
+        c = oracle.condense(w.elem_ne[:m], w.elem_nf[:m], blk)
+        f1 = int(np.searchsorted(w.face_elem[:, 0], m))      # faces whose left element is in the sample
+        sym = oracle.symbolic(w.elem_face, w.face_elem, w.face_ndof, 0, f1)
+        oracle.assemble(w.elem_face, w.face_ndof, w.face_off, w.elem_nf[:m], c["S"], c["off_S"], c["g"],
+                        c["off_g"], sym, 0, f1, 0, m)
+        oracle.backsub(w.elem_face, w.face_ndof, w.face_off, w.elem_ne[:m], w.elem_nf[:m], c["LU"], c["off_LU"],
+                       c["piv"], c["off_piv"], blk["B"], blk["off_B"], blk["re"], blk["off_re"], lam)
+        return time.perf_counter() - t0
+
+    m = min(64, w.E)
+    t = run(m)
+    m2 = int(min(w.E, max(m, m * seconds / max(t, 1e-6))))
+    if max_elems:
+        m2 = min(m2, max_elems)
+    t2 = run(m2)
+    threads = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    return m2 / t2, m2, t2, threads
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (the only reference this tier has) on the box's host cores."""
+    if rank != 0:
+        return
+    import gen
+    w = gen.config(args.config)
+    lam = gen.host_lambda(w)
+    for _ in range(args.warmup):
+        oracle_sample(w, args.ref_seconds / 4, lam, max_elems=4096)
+    vals, ms, secs = [], [], []
+    for _ in range(args.steps):
+        v, m, t, threads = oracle_sample(w, args.ref_seconds, lam)
+        vals.append(v)
+        ms.append(m)
+        secs.append(t)
+    value = float(np.median(vals))
+    sample = (f"first {ms[-1]} of {w.E} elements of {args.config} per step: oracle condense + assemble (rows owned "
+              f"by the sample) + back-substitute, {np.mean(secs):.1f} s per step, generation excluded")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * w.E / value,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Philox blocks, BASELINE.json distributions)",
+            "config": {"workload": args.config, "elements": w.E, "n_e": int(w.elem_ne.max()),
+                       "n_f": int(w.elem_nf.max())},
+            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hdg", choices=["hdg", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import gen
+    import paper_1308_3995_b200 as hdg
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    dmma_peak, dfma_peak = (fp64_peak_in_run() if rank == 0 else (None, None))
+
+    w = gen.config(args.config)
+    reb = slab_bounds(w.E, world)
+    eb, n = int(reb[rank]), int(reb[rank + 1] - reb[rank])
+    ctx = hdg.Context(local, rank, world)
+    info = ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne, eb, n, reb if world > 1 else None)
+    stream = torch.cuda.Stream(dev)
+
+    # inputs generated in HBM for this rank's slab (same bytes as gen.host_blocks)
+    inp = {}
+    with torch.cuda.stream(stream):
+        dne = torch.from_numpy(w.elem_ne[eb:eb + n].copy()).to(dev)
+        dnf = torch.from_numpy(w.elem_nf[eb:eb + n].copy()).to(dev)
+        for k in ("A", "B", "C", "D", "re", "rf"):
+            o = w.off[k][eb:eb + n + 1] - w.off[k][eb]
+            inp[k] = torch.empty(max(int(o[-1]), 2), dtype=torch.float64, device=dev)
+            if w.uniform:
+                gen.device_blocks(w, k, inp[k], e0=eb, n=n, stream=stream.cuda_stream)
+            else:
+                gen.device_blocks(w, k, inp[k], e0=eb, n=n, off=torch.from_numpy(o).to(dev), stream=stream.cuda_stream,
+                                  dev_ne=dne, dev_nf=dnf)
+        lam = torch.empty(w.n_trace, dtype=torch.float64, device=dev)
+        gen.device_lambda(w, lam, torch.from_numpy(w.face_ndof).to(dev), torch.from_numpy(w.face_off).to(dev))
+    S, g, u = ctx.alloc("S"), ctx.alloc("g"), ctx.alloc("u")
+    F, infot = ctx.alloc("factors"), ctx.alloc("info")
+    K, E = ctx.alloc("K"), ctx.alloc("E")
+    send = ctx.alloc("send") if info.send_doubles > 0 else None
+    recv = ctx.alloc("recv") if info.recv_doubles > 0 else None
+    torch.cuda.synchronize()
+
+    launches = [0]
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], S, g, F, infot, stream=stream)
+        launches[0] += ctx.launch_count()
+        if ev:
+            ev[1].record(stream)
+        ctx.assemble_skeleton(S, g, K, E, send=send, stream=stream)
+        launches[0] += ctx.launch_count()
+        if world > 1:
+            stream.synchronize()
+            hdg.exchange(ctx, send, recv)
+            ctx.skeleton_accumulate(recv, K, E, stream=stream)
+            launches[0] += ctx.launch_count()
+        if ev:
+            ev[2].record(stream)
+        ctx.backsubstitute(F, inp["B"], inp["re"], lam, u, stream=stream)
+        launches[0] += ctx.launch_count()
+        if ev:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    bad, code = ctx.first_error(infot, stream=stream)
+    if bad >= 0:
+        raise RuntimeError(f"singular element {bad} (info {code}) in the benchmark inputs")
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    launches[0] = 0
+    t0.record(stream)
+    for i in range(args.steps):
+        step(evs[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    total_ms = t0.elapsed_time(t1)
+    cond_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    asm_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    bs_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    gpu_launches = launches[0]
+    t = torch.tensor([total_ms, cond_ms, asm_ms, bs_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, cond_ms, asm_ms, bs_ms = t.tolist()
+    ms_step = total_ms / args.steps
+
+    # ---- e2e: the same step through the public API with HOST buffers (pinned), copies inside the timed region ----
+    e2e = None
+    if not args.no_e2e:
+        host = {k: torch.empty(v.numel(), dtype=v.dtype, pin_memory=True) for k, v in inp.items()}
+        for k in host:
+            host[k].copy_(inp[k])
+        hlam = torch.empty(lam.numel(), dtype=torch.float64, pin_memory=True)
+        hlam.copy_(lam)
+        hu = torch.empty(u.numel(), dtype=torch.float64, pin_memory=True)
+        hK = torch.empty(K.numel(), dtype=torch.float64, pin_memory=True)
+        hE = torch.empty(E.numel(), dtype=torch.float64, pin_memory=True)
+        h2d = sum(v.numel() * 8 for v in host.values()) + hlam.numel() * 8
+        d2h = (hu.numel() + hK.numel() + hE.numel()) * 8
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                for k in host:
+                    inp[k].copy_(host[k], non_blocking=True)
+                lam.copy_(hlam, non_blocking=True)
+            step()
+            with torch.cuda.stream(stream):
+                hK.copy_(K, non_blocking=True)
+                hE.copy_(E, non_blocking=True)
+                hu.copy_(u, non_blocking=True)
+
+        ke2e = max(1, min(args.steps, 3))
+        e2e_step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        a.record(stream)
+        for _ in range(ke2e):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b) / ke2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": w.E / (te.item() / 1e3), "unit": "elements/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": ke2e,
+               "note": "host (pinned) inputs A,B,C,D,r_e,r_f,lambda copied in and K,E,u copied out every step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, m, secs, threads = oracle_sample(w, args.cpu_seconds, gen.host_lambda(w))
+        cpu = {"value": v, "unit": "elements/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {m} of {w.E} elements: oracle condense + assemble (rows owned by the sample) + "
+                         f"back-substitute, {secs:.1f} s wall, generation excluded"}
+
+    if rank == 0:
+        work = algorithmic(w.elem_ne[eb:eb + n], w.elem_nf[eb:eb + n])
+        peaks = measured_peaks()
+        hbm = peaks.get("hbm_gbs")
+        cond_tflops = work["condense_flops"] / (cond_ms * 1e-3) / 1e12
+        cond_gbs = work["condense_bytes"] / (cond_ms * 1e-3) / 1e9
+        fp64_peak = dmma_peak or 37.2
+        t_fp = work["condense_flops"] / (fp64_peak * 1e12)
+        t_hbm = work["condense_bytes"] / ((hbm or 6551.4) * 1e9)
+        if t_fp >= t_hbm:
+            roof = {"bound": "tensor", "achieved": cond_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": cond_tflops / fp64_peak, "traffic": None,
+                    "kernel": "condense_kernel (hdg_condense)", "dtype": "f64 (DMMA m8n8k4 + DFMA)",
+                    "peak_source": ("FP64 DMMA peak measured in this run by tools/peaks (K9)" if dmma_peak else
+                                    "nominal 148 SM x 64 FP64 FMA/clk x 1.965 GHz (no in-run measurement)"),
+                    "flops_per_launch": work["condense_flops"],
+                    "hbm_achieved_gbs": cond_gbs, "hbm_frac": cond_gbs / (hbm or 6551.4)}
+        else:
+            roof = {"bound": "hbm", "achieved": cond_gbs, "peak": hbm or 6551.4, "unit": "GB/s",
+                    "frac": cond_gbs / (hbm or 6551.4), "traffic": None, "kernel": "condense_kernel (hdg_condense)",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6551.4",
+                    "bytes_per_launch": work["condense_bytes"], "fp64_tflops": cond_tflops}
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            roof["traffic"] = tr.get(args.config)
+        except Exception:
+            pass
+        line = {
+            "metric": METRIC, "value": w.E / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Philox blocks with BASELINE.json distributions, generated in HBM)",
+            "config": {"workload": args.config, "elements": w.E, "n_e": int(w.elem_ne.max()),
+                       "n_f": int(w.elem_nf.max()), "faces": w.F, "trace_dofs": w.n_trace,
+                       "parallelism": f"element slabs x{world}" + (" + NCCL shared-face exchange" if world > 1 else ""),
+                       "l2": "inputs (%.1f GB/rank) exceed the 126 MB L2; no flush needed" % (
+                           sum(v.numel() for v in inp.values()) * 8 / 1e9),
+                       "step": "condense + assemble_skeleton + backsubstitute"},
+            "condense_per_s": w.E / (cond_ms * 1e-3), "backsub_per_s": w.E / (bs_ms * 1e-3),
+            "condense_ms": cond_ms, "assemble_ms": asm_ms, "backsub_ms": bs_ms,
+            "backsub_hbm_gbs": work["backsub_bytes"] / (bs_ms * 1e-3) / 1e9,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+            "fp64_peak_tflops": {"dmma": dmma_peak, "dfma": dfma_peak},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+/* include/hdg.h — C ABI of libhdg: element-local static condensation and its inverse on B200 (sm_100a), fp64.
+ *
+ * The operations are those of the paper's hybridization (§3.4):
+ * the linearised HDG system Eq. 44 [[A B R],[C D S],[L M N]] [dQ dW dL] = [F G H] is split into
+ * element-local equations (Eq. ls) and the trace equations (Eq. cons);
+ * eliminating the element unknowns yields the hybridized system K dL = E (Eq. hybridsystem).
+ * The local matrix is block-diagonal by element, so everything is element-wise.
+ *
+ * Notation: per element e,
+ *   A_e  (n_e x n_e)  = [[A,B],[C,D]] restricted to e          (paper's local matrix)
+ *   B_e  (n_e x n_f)  = [R;S] restricted to e's rows, e's trace columns
+ *   C_e  (n_f x n_e)  = [L M] restricted to e's trace rows, e's columns
+ *   D_e  (n_f x n_f)  = e's contribution to N
+ *   r_e  (n_e), r_f (n_f) = [F;G]|_e and e's contribution to H
+ *   S_e = D_e - C_e A_e^-1 B_e,  g_e = r_f - C_e A_e^-1 r_e       (e's contributions to K and E)
+ *   u_e = A_e^-1 (r_e - B_e lambda_e)                            (reconstruction, Eq. ls)
+ * n_e = element unknowns, n_f = sum over the element's three face slots of the face's trace size (0 for a slot
+ * of -1). Trace columns/rows of an element are ordered slot 0, 1, 2, each face's dofs contiguous, in the face's
+ * global dof order.
+ *
+ * Memory conventions:
+ *   - All array arguments of the compute calls are CUDA DEVICE pointers owned by the caller, except where
+ *     marked [host]. The library allocates only its own context/plan workspace (freed by hdg_ctx_destroy).
+ *   - Element blocks are row-major and packed densely in local element order, without gaps: block X of local
+ *     element l starts at sum_{l' < l} size_X(l') doubles (size_A = n_e^2, size_B = n_e n_f, size_C = n_f n_e,
+ *     size_D = n_f^2, size_re = n_e, size_rf = n_f, size_S = n_f^2, size_g = n_f, size_u = n_e).
+ *     Every base pointer must be 16-byte aligned. hdg_plan reports each array's total length.
+ *   - lambda and E are indexed by trace dof: face f's dofs occupy [face_off[f], face_off[f] + face_ndof[f]),
+ *     face_off = exclusive prefix sum of face_ndof over global face ids.
+ *   - Every compute call is stream-ordered and asynchronous on the given stream; argument errors are detected
+ *     synchronously before any launch and return HDG_ERR_ARG with nothing launched.
+ *   - Threading: a context is used by one host thread at a time; one context per device.
+ *   - Errors: hdg_status codes, never exceptions; hdg_last_error(ctx) holds a message for the last failure.
+ *     Numerical failure is reported per element in info[] (LAPACK getrf convention), see hdg_condense.
+ */
+#ifndef HDG_H
+#define HDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hdg_ctx_s* hdg_ctx;
+typedef void* hdg_stream; /* a cudaStream_t (NULL = legacy default stream) */
+
+typedef enum {
+  HDG_OK = 0,
+  HDG_ERR_ARG = 1,         /* bad argument / shape / alignment; nothing launched */
+  HDG_ERR_SINGULAR = 2,    /* hdg_first_error found an element with info != 0 */
+  HDG_ERR_CUDA = 3,        /* CUDA runtime error (message in hdg_last_error) */
+  HDG_ERR_NOMEM = 4,       /* workspace allocation failed */
+  HDG_ERR_STATE = 5,       /* call out of order (e.g. compute before hdg_plan) */
+  HDG_ERR_UNSUPPORTED = 6  /* sizes outside what this build supports (n_e > 256, n_f > 96, ...) */
+} hdg_status;
+
+/* Library version and the supported maxima. */
+const char* hdg_version(void);
+int hdg_max_elem_ndof(void);   /* largest n_e supported by the condensation kernels */
+int hdg_max_face_ndof(void);   /* largest n_f (element trace size) supported */
+
+const char* hdg_status_string(hdg_status s);
+
+/* Context on CUDA device `device` for rank `rank` of `nranks` (element-slab partition; see hdg_mesh).
+ * [host] out. The context owns the plan and all workspace. */
+hdg_status hdg_ctx_create(hdg_ctx* out, int device, int rank, int nranks);
+void hdg_ctx_destroy(hdg_ctx ctx);
+const char* hdg_last_error(hdg_ctx ctx);
+
+/* The mesh skeleton and degree map (§3.1): all pointers [host], global ids throughout.
+ * Faces are the element edges carrying trace unknowns; a slot of -1 carries none (e.g. the paper's boundary
+ * edges). This rank owns elements [elem_begin, elem_begin + n_elem). A face row of K is
+ * owned by the rank of its left (lower-id) element; owned faces must form a contiguous id range. */
+typedef struct {
+  int64_t n_elem_global;     /* E */
+  int64_t n_face;            /* F */
+  int64_t elem_begin;        /* first element of this rank's slab */
+  int64_t n_elem;            /* elements of this rank's slab */
+  const int32_t* elem_face;  /* [E][3] face id per slot, or -1 */
+  const int32_t* face_elem;  /* [F][2] (left, right), left < right; right = -1 for a one-sided face */
+  const int32_t* face_ndof;  /* [F] trace dofs of the face, m (p_f + 1) */
+  const int32_t* elem_ndof;  /* [E] n_e of each element */
+  const int64_t* rank_elem_begin; /* [nranks + 1] slab boundaries (NULL iff nranks == 1) */
+} hdg_mesh;
+
+typedef struct {
+  int64_t n_elem;                       /* local elements */
+  int64_t len_A, len_B, len_C, len_D;   /* doubles of each packed input array */
+  int64_t len_re, len_rf;
+  int64_t len_S, len_g, len_u;          /* doubles of each packed output array */
+  int64_t factor_bytes;                 /* size of the opaque factor buffer */
+  int64_t owned_face_begin, n_owned_faces;   /* rows of K stored on this rank */
+  int64_t nnzb;                         /* blocks in the owned rows (col_idx length) */
+  int64_t nvals;                        /* doubles of K (blk_off[nnzb]) */
+  int64_t owned_trace_begin, n_owned_trace;  /* E covers trace dofs [begin, begin + n) */
+  int64_t n_trace;                      /* global trace dofs (length of lambda) */
+  int32_t n_buckets;                    /* distinct (n_e, n_f) classes among local elements */
+  int32_t max_ne, max_nf;
+  int64_t send_doubles, recv_doubles;   /* exchange buffer sizes (0 when nranks == 1) */
+} hdg_plan_info;
+
+/* a0 plan (once per mesh and degree map): validates the mesh, buckets local elements by (n_e, n_f) (the hp
+ * degree classes), computes packed offsets, builds the block-CSR structure of the owned skeleton rows on the
+ * device (row_ptr/col_idx/blk_off) and the exchange lists for faces shared between slabs.
+ * Synchronizes `stream`. Replaces any previous plan of the context. [host] info. */
+hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* mesh, hdg_plan_info* info, hdg_stream stream);
+
+/* a1-a5 condensation (Eq. hybridsystem): for every local element, factor A_e with partial
+ * pivoting and form S_e = D_e - C_e A_e^-1 B_e, g_e = r_f - C_e A_e^-1 r_e.
+ * Inputs A, B, C, D, r_e, r_f: packed as above (read only). Outputs S, g: packed. factors: opaque buffer of
+ * plan.factor_bytes bytes holding the element factorizations for hdg_backsubstitute ("can be saved ... and
+ * reused during the reconstruction"). info: int32 [n_elem]; info[l] = 0 on success, or k+1 if
+ * the k-th pivot of element l was exactly zero, in which case S_l and g_l are set to NaN. */
+hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                        const double* r_e, const double* r_f, double* S, double* g, void* factors,
+                        int32_t* info, hdg_stream stream);
+
+/* a6 (+a7 pack) assembly of the owned skeleton rows: K[f, f'] = sum over local elements e adjacent to both of
+ * S_e[slot(f), slot(f')], E[f] = sum of g_e[slot(f)], contributions taken left (lower element id) then right
+ * (SURVEY.md S10). Block-CSR over owned rows: row_ptr [n_owned_faces + 1] int32 (block
+ * counts, 0-based), col_idx [nnzb] int32 global face ids ascending (diagonal included), blk_off [nnzb + 1]
+ * int64 offsets of each row-major n_fp(row) x n_fp(col) block in K (doubles), K [nvals], E [n_owned_trace].
+ * row_ptr/col_idx/blk_off may be NULL (structure not copied out; it is fixed by the plan).
+ * With nranks > 1, send (device, plan.send_doubles) receives this rank's contributions to face rows owned by
+ * other ranks; exchange it with hdg_exchange_counts' layout and finish with hdg_skeleton_accumulate. */
+hdg_status hdg_assemble_skeleton(hdg_ctx ctx, const double* S, const double* g, int32_t* row_ptr,
+                                 int32_t* col_idx, int64_t* blk_off, double* K, double* E, double* send,
+                                 hdg_stream stream);
+
+/* a7 exchange layout: per peer rank, doubles sent/received and their offsets in send/recv [host, nranks]. */
+hdg_status hdg_exchange_counts(hdg_ctx ctx, int64_t* send_counts, int64_t* send_displs, int64_t* recv_counts,
+                               int64_t* recv_displs);
+
+/* a7 finish: add the contributions received from other ranks (recv, device, plan.recv_doubles) into the owned
+ * rows, after this rank's own (left) contributions: the result is bitwise identical to one rank. */
+hdg_status hdg_skeleton_accumulate(hdg_ctx ctx, const double* recv, double* K, double* E, hdg_stream stream);
+
+/* a8 back-substitution (Eq. ls): u_e = A_e^-1 (r_e - B_e lambda_e) for every local
+ * element, with lambda_e gathered from the global trace vector lambda [n_trace] (device) in slot order.
+ * factors: from hdg_condense on the same plan. B, r_e: the packed inputs of hdg_condense. u: packed output. */
+hdg_status hdg_backsubstitute(hdg_ctx ctx, const void* factors, const double* B, const double* r_e,
+                              const double* lambda, double* u, hdg_stream stream);
+
+/* Lowest local element with info != 0 (synchronizes stream). Returns HDG_OK with *elem = -1 if none, or
+ * HDG_ERR_SINGULAR with the element (local index) and its info code ("singular local block -> diagnostic
+ * naming the element"). */
+hdg_status hdg_first_error(hdg_ctx ctx, const int32_t* info, int64_t* elem, int32_t* code, hdg_stream stream);
+
+/* Kernel launches issued by the last hdg_condense / hdg_assemble_skeleton(+accumulate) / hdg_backsubstitute
+ * calls of this context (instrumentation for the benchmark's launch count). */
+int64_t hdg_launch_count(hdg_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDG_H */

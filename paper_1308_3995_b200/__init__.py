@@ -1,0 +1,278 @@
+"""paper_1308_3995_b200 — B200-native static condensation for hybridized DG (arXiv 1308.3995, §3.4).
+
+Thin Python binding of libhdg.so (the C ABI in include/hdg.h): argument marshalling only. Every step of the hot
+path — condensation (LU with partial pivoting, local solves, Schur complement), skeleton assembly (block-CSR,
+left-then-right sums), the shared-face exchange pack/accumulate and the back-substitution — runs in the
+library's sm_100a CUDA kernels. PyTorch supplies device memory, streams and torch.distributed (plumbing only).
+
+There is no CPU fallback: if libhdg.so is missing or no sm_100 device is present, every call raises.
+
+Names follow the paper: K, E (Eq. hybridsystem), lambda (the trace unknowns dLambda), and the
+per-element blocks A_e, B_e, C_e, D_e, r_e, r_f, S_e, g_e, u_e of SURVEY.md §0.1.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhdg.so")
+
+HDG_OK, HDG_ERR_ARG, HDG_ERR_SINGULAR, HDG_ERR_CUDA, HDG_ERR_NOMEM, HDG_ERR_STATE, HDG_ERR_UNSUPPORTED = range(7)
+
+
+class HDGError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libhdg status {status}: {msg}")
+        self.status = status
+
+
+class _Mesh(ctypes.Structure):
+    _fields_ = [("n_elem_global", ctypes.c_int64), ("n_face", ctypes.c_int64), ("elem_begin", ctypes.c_int64),
+                ("n_elem", ctypes.c_int64), ("elem_face", ctypes.c_void_p), ("face_elem", ctypes.c_void_p),
+                ("face_ndof", ctypes.c_void_p), ("elem_ndof", ctypes.c_void_p),
+                ("rank_elem_begin", ctypes.c_void_p)]
+
+
+class _PlanInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "n_elem", "len_A", "len_B", "len_C", "len_D", "len_re", "len_rf", "len_S", "len_g", "len_u",
+        "factor_bytes", "owned_face_begin", "n_owned_faces", "nnzb", "nvals", "owned_trace_begin",
+        "n_owned_trace", "n_trace")] + [("n_buckets", ctypes.c_int32), ("max_ne", ctypes.c_int32),
+                                        ("max_nf", ctypes.c_int32), ("send_doubles", ctypes.c_int64),
+                                        ("recv_doubles", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhdg.so. Raises if the extension has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libhdg.so not built ({LIB_PATH}); run __graft_entry__.build() or "
+                              f"python paper_1308_3995_b200/build.py")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.hdg_version.restype = ctypes.c_char_p
+        L.hdg_status_string.restype = ctypes.c_char_p
+        L.hdg_status_string.argtypes = [I32]
+        L.hdg_ctx_create.restype = I32
+        L.hdg_ctx_create.argtypes = [ctypes.POINTER(P), I32, I32, I32]
+        L.hdg_ctx_destroy.argtypes = [P]
+        L.hdg_last_error.restype = ctypes.c_char_p
+        L.hdg_last_error.argtypes = [P]
+        L.hdg_plan.restype = I32
+        L.hdg_plan.argtypes = [P, ctypes.POINTER(_Mesh), ctypes.POINTER(_PlanInfo), P]
+        L.hdg_condense.restype = I32
+        L.hdg_condense.argtypes = [P] + [P] * 10 + [P]
+        L.hdg_assemble_skeleton.restype = I32
+        L.hdg_assemble_skeleton.argtypes = [P] + [P] * 8 + [P]
+        L.hdg_exchange_counts.restype = I32
+        L.hdg_exchange_counts.argtypes = [P, P, P, P, P]
+        L.hdg_skeleton_accumulate.restype = I32
+        L.hdg_skeleton_accumulate.argtypes = [P, P, P, P, P]
+        L.hdg_backsubstitute.restype = I32
+        L.hdg_backsubstitute.argtypes = [P] + [P] * 5 + [P]
+        L.hdg_first_error.restype = I32
+        L.hdg_first_error.argtypes = [P, P, ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_int32), P]
+        L.hdg_launch_count.restype = I64
+        L.hdg_launch_count.argtypes = [P]
+        L.hdg_max_elem_ndof.restype = I32
+        L.hdg_max_face_ndof.restype = I32
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status_string", "hdg_ctx_create",
+            "hdg_ctx_destroy", "hdg_last_error", "hdg_plan", "hdg_condense", "hdg_assemble_skeleton",
+            "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
+            "hdg_launch_count")
+
+
+def _ptr(t):
+    if t is None:
+        return ctypes.c_void_p(0)
+    import torch
+    if isinstance(t, torch.Tensor):
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        if not t.is_cuda:
+            raise ValueError("tensor must live on the CUDA device (libhdg takes device pointers)")
+        return ctypes.c_void_p(t.data_ptr())
+    raise TypeError(type(t))
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _f64(*ts):
+    import torch
+    for t in ts:
+        if t is not None and t.dtype != torch.float64:
+            raise TypeError("fp64 tensors required")
+
+
+@dataclass
+class PlanInfo:
+    n_elem: int
+    len_A: int
+    len_B: int
+    len_C: int
+    len_D: int
+    len_re: int
+    len_rf: int
+    len_S: int
+    len_g: int
+    len_u: int
+    factor_bytes: int
+    owned_face_begin: int
+    n_owned_faces: int
+    nnzb: int
+    nvals: int
+    owned_trace_begin: int
+    n_owned_trace: int
+    n_trace: int
+    n_buckets: int
+    max_ne: int
+    max_nf: int
+    send_doubles: int
+    recv_doubles: int
+
+
+class Context:
+    """One libhdg context (device, rank of nranks). Mirrors include/hdg.h call for call."""
+
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1):
+        self._L = lib()
+        h = ctypes.c_void_p()
+        st = self._L.hdg_ctx_create(ctypes.byref(h), device, rank, nranks)
+        if st != HDG_OK:
+            raise HDGError(st, f"hdg_ctx_create(device={device}): {self._L.hdg_status_string(st).decode()}")
+        self._h = h
+        self.device, self.rank, self.nranks = device, rank, nranks
+        self.info: PlanInfo | None = None
+        self._keep = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.hdg_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int, what: str):
+        if st != HDG_OK:
+            raise HDGError(st, f"{what}: {self._L.hdg_last_error(self._h).decode()}")
+
+    # -- a0 ------------------------------------------------------------------------------------------------------
+    def plan(self, elem_face, face_elem, face_ndof, elem_ndof, elem_begin: int = 0, n_elem: int | None = None,
+             rank_elem_begin=None, stream=None) -> PlanInfo:
+        ef = np.ascontiguousarray(elem_face, dtype=np.int32)
+        fe = np.ascontiguousarray(face_elem, dtype=np.int32)
+        fn = np.ascontiguousarray(face_ndof, dtype=np.int32)
+        en = np.ascontiguousarray(elem_ndof, dtype=np.int32)
+        E = ef.shape[0]
+        if n_elem is None:
+            n_elem = E - elem_begin
+        rb = None if rank_elem_begin is None else np.ascontiguousarray(rank_elem_begin, dtype=np.int64)
+        m = _Mesh(E, fe.shape[0], elem_begin, n_elem, ef.ctypes.data, fe.ctypes.data, fn.ctypes.data, en.ctypes.data,
+                  rb.ctypes.data if rb is not None else None)
+        pi = _PlanInfo()
+        self._check(self._L.hdg_plan(self._h, ctypes.byref(m), ctypes.byref(pi), _stream(stream)), "hdg_plan")
+        self.info = PlanInfo(**{k: getattr(pi, k) for k, _ in _PlanInfo._fields_})
+        return self.info
+
+    def alloc(self, what: str):
+        """Allocate a correctly sized device output: 'S', 'g', 'u', 'factors', 'info', 'K', 'E', 'row_ptr',
+        'col_idx', 'blk_off', 'send', 'recv'."""
+        import torch
+        i, dev = self.info, torch.device("cuda", self.device)
+        f64 = dict(dtype=torch.float64, device=dev)
+        sizes = {"S": i.len_S, "g": i.len_g, "u": i.len_u, "K": i.nvals, "E": i.n_owned_trace,
+                 "send": i.send_doubles, "recv": i.recv_doubles}
+        if what in sizes:
+            return torch.empty(max(sizes[what], 1), **f64)
+        if what == "factors":
+            return torch.empty(max(i.factor_bytes, 16), dtype=torch.uint8, device=dev)
+        if what == "info":
+            return torch.empty(max(i.n_elem, 1), dtype=torch.int32, device=dev)
+        if what == "row_ptr":
+            return torch.empty(i.n_owned_faces + 1, dtype=torch.int32, device=dev)
+        if what == "col_idx":
+            return torch.empty(max(i.nnzb, 1), dtype=torch.int32, device=dev)
+        if what == "blk_off":
+            return torch.empty(i.nnzb + 1, dtype=torch.int64, device=dev)
+        raise KeyError(what)
+
+    # -- a1-a5 ---------------------------------------------------------------------------------------------------
+    def condense(self, A, B, C, D, r_e, r_f, S, g, factors, info, stream=None):
+        _f64(A, B, C, D, r_e, r_f, S, g)
+        self._check(self._L.hdg_condense(self._h, *map(_ptr, (A, B, C, D, r_e, r_f, S, g, factors, info)),
+                                         _stream(stream)), "hdg_condense")
+
+    # -- a6 / a7 ---------------------------------------------------------------------------------------------------
+    def assemble_skeleton(self, S, g, K, E, row_ptr=None, col_idx=None, blk_off=None, send=None, stream=None):
+        _f64(S, g, K, E, send)
+        self._check(self._L.hdg_assemble_skeleton(self._h, *map(_ptr, (S, g, row_ptr, col_idx, blk_off, K, E, send)),
+                                                  _stream(stream)), "hdg_assemble_skeleton")
+
+    def exchange_counts(self):
+        n = self.nranks
+        arrs = [np.zeros(n, dtype=np.int64) for _ in range(4)]
+        self._check(self._L.hdg_exchange_counts(self._h, *[ctypes.c_void_p(a.ctypes.data) for a in arrs]),
+                    "hdg_exchange_counts")
+        return tuple(arrs)
+
+    def skeleton_accumulate(self, recv, K, E, stream=None):
+        _f64(recv, K, E)
+        self._check(self._L.hdg_skeleton_accumulate(self._h, _ptr(recv), _ptr(K), _ptr(E), _stream(stream)),
+                    "hdg_skeleton_accumulate")
+
+    # -- a8 ----------------------------------------------------------------------------------------------------------
+    def backsubstitute(self, factors, B, r_e, lam, u, stream=None):
+        _f64(B, r_e, lam, u)
+        self._check(self._L.hdg_backsubstitute(self._h, *map(_ptr, (factors, B, r_e, lam, u)), _stream(stream)),
+                    "hdg_backsubstitute")
+
+    def first_error(self, info, stream=None):
+        e = ctypes.c_int64()
+        c = ctypes.c_int32()
+        st = self._L.hdg_first_error(self._h, _ptr(info), ctypes.byref(e), ctypes.byref(c), _stream(stream))
+        if st not in (HDG_OK, HDG_ERR_SINGULAR):
+            self._check(st, "hdg_first_error")
+        return e.value, c.value
+
+    def launch_count(self) -> int:
+        return int(self._L.hdg_launch_count(self._h))
+
+
+def exchange(ctx: Context, send, recv, group=None):
+    """a7 transport: ship each rank's packed shared-face contributions to the owning ranks with
+    torch.distributed point-to-point ops (NCCL over NVLink on GPUs). Plumbing only — packing and the ordered
+    accumulation run in libhdg's kernels (hdg_assemble_skeleton / hdg_skeleton_accumulate)."""
+    import torch.distributed as dist
+    sc, sd, rc, rd = ctx.exchange_counts()
+    ops = []
+    for r in range(ctx.nranks):
+        if r == ctx.rank:
+            continue
+        if rc[r] > 0:
+            ops.append(dist.P2POp(dist.irecv, recv[rd[r]:rd[r] + rc[r]], r, group))
+        if sc[r] > 0:
+            ops.append(dist.P2POp(dist.isend, send[sd[r]:sd[r] + sc[r]], r, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()

@@ -1,0 +1,426 @@
+// api.cu — the C ABI of libhdg (include/hdg.h): context, plan (row a0), argument checking and dispatch of the
+// condensation (a1-a5), skeleton assembly / exchange (a6-a7) and back-substitution (a8) kernels.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <tuple>
+
+#include "hdg_internal.cuh"
+
+using namespace hdg;
+
+namespace {
+
+const char* kVersion = "libhdg 0.1 (sm_100a, fp64)";
+
+hdg_status fail(hdg_ctx ctx, hdg_status st, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    ctx->last_error = buf;
+  }
+  return st;
+}
+
+hdg_status cuda_fail(hdg_ctx ctx, cudaError_t e, const char* where) {
+  return fail(ctx, HDG_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define HDG_CUDA(ctx, call)                                    \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call);   \
+  } while (0)
+
+template <class T>
+cudaError_t upload(T** dst, const T* src, size_t n) {
+  cudaError_t e = cudaMalloc(dst, sizeof(T) * (n > 0 ? n : 1));
+  if (e != cudaSuccess) return e;
+  if (n > 0) e = cudaMemcpy(*dst, src, sizeof(T) * n, cudaMemcpyHostToDevice);
+  return e;
+}
+
+void free_plan(Plan& p) {
+  cudaFree(p.d_elem_face); cudaFree(p.d_face_elem); cudaFree(p.d_face_ndof); cudaFree(p.d_face_off);
+  cudaFree(p.d_ne); cudaFree(p.d_nf);
+  for (auto& o : p.d_off) cudaFree(o);
+  for (auto& b : p.buckets) cudaFree(b.d_elems);
+  cudaFree(p.sk.d_row_ptr); cudaFree(p.sk.d_col_idx); cudaFree(p.sk.d_blk_off); cudaFree(p.sk.d_blk_row);
+  cudaFree(p.sk.d_send_items); cudaFree(p.sk.d_recv_items);
+  cudaFree(p.d_scratch);
+  p = Plan();
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* hdg_version(void) { return kVersion; }
+int hdg_max_elem_ndof(void) { return kMaxNe; }
+int hdg_max_face_ndof(void) { return kMaxNf; }
+
+const char* hdg_status_string(hdg_status s) {
+  switch (s) {
+    case HDG_OK: return "ok";
+    case HDG_ERR_ARG: return "invalid argument";
+    case HDG_ERR_SINGULAR: return "singular local block";
+    case HDG_ERR_CUDA: return "CUDA error";
+    case HDG_ERR_NOMEM: return "out of memory";
+    case HDG_ERR_STATE: return "invalid state";
+    case HDG_ERR_UNSUPPORTED: return "unsupported size";
+  }
+  return "unknown status";
+}
+
+hdg_status hdg_ctx_create(hdg_ctx* out, int device, int rank, int nranks) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return HDG_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return HDG_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return HDG_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return HDG_ERR_CUDA;
+  if (prop.major != 10) return HDG_ERR_UNSUPPORTED;   // built for sm_100a only
+  hdg_ctx c = new hdg_ctx_s;
+  c->device = device;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->sms = prop.multiProcessorCount;
+  c->smem_optin = prop.sharedMemPerBlockOptin;
+  *out = c;
+  return HDG_OK;
+}
+
+void hdg_ctx_destroy(hdg_ctx ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  free_plan(ctx->plan);
+  delete ctx;
+}
+
+const char* hdg_last_error(hdg_ctx ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int64_t hdg_launch_count(hdg_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  if (!m || !info || !m->elem_face || !m->face_elem || !m->face_ndof || !m->elem_ndof)
+    return fail(ctx, HDG_ERR_ARG, "hdg_plan: null mesh array");
+  const int64_t E = m->n_elem_global, F = m->n_face, eb = m->elem_begin, n = m->n_elem;
+  if (E < 0 || F < 0 || eb < 0 || n < 0 || eb + n > E || E > INT32_MAX || F > INT32_MAX)
+    return fail(ctx, HDG_ERR_ARG, "hdg_plan: bad sizes E=%lld F=%lld begin=%lld n=%lld", (long long)E, (long long)F,
+                (long long)eb, (long long)n);
+  if (ctx->nranks > 1) {
+    if (!m->rank_elem_begin) return fail(ctx, HDG_ERR_ARG, "hdg_plan: rank_elem_begin required for nranks > 1");
+    if (m->rank_elem_begin[ctx->rank] != eb || m->rank_elem_begin[ctx->rank + 1] != eb + n ||
+        m->rank_elem_begin[0] != 0 || m->rank_elem_begin[ctx->nranks] != E)
+      return fail(ctx, HDG_ERR_ARG, "hdg_plan: rank_elem_begin inconsistent with elem_begin/n_elem");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  free_plan(ctx->plan);
+  Plan& p = ctx->plan;
+  p.E = E; p.F = F; p.eb = eb; p.n = n;
+
+  // ---- validate connectivity ---------------------------------------------------------------------------------
+  for (int64_t f = 0; f < F; ++f) {
+    const int32_t l = m->face_elem[2 * f], r = m->face_elem[2 * f + 1];
+    if (l < 0 || l >= E || r >= E || (r >= 0 && r <= l))
+      return fail(ctx, HDG_ERR_ARG, "hdg_plan: face %lld has bad (left,right) = (%d,%d)", (long long)f, l, r);
+    const int32_t nd = m->face_ndof[f];
+    if (nd <= 0 || (nd & 1)) return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_plan: face %lld trace size %d (must be even, > 0)", (long long)f, nd);
+  }
+  std::vector<int64_t> face_off(F + 1, 0);
+  for (int64_t f = 0; f < F; ++f) face_off[f + 1] = face_off[f] + m->face_ndof[f];
+  p.n_trace = face_off[F];
+
+  std::vector<int32_t> ne(n), nf(n);
+  for (int64_t l = 0; l < n; ++l) {
+    const int64_t e = eb + l;
+    int t = 0;
+    for (int k = 0; k < 3; ++k) {
+      const int32_t f = m->elem_face[3 * e + k];
+      if (f < -1 || f >= F) return fail(ctx, HDG_ERR_ARG, "hdg_plan: element %lld slot %d face %d out of range", (long long)e, k, f);
+      if (f >= 0) {
+        if (m->face_elem[2 * f] != e && m->face_elem[2 * f + 1] != e)
+          return fail(ctx, HDG_ERR_ARG, "hdg_plan: element %lld lists face %d which does not list it", (long long)e, f);
+        t += m->face_ndof[f];
+      }
+    }
+    ne[l] = m->elem_ndof[e];
+    nf[l] = t;
+    if (ne[l] <= 0 || (ne[l] & 3)) return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_plan: element %lld n_e=%d (must be a positive multiple of 4)", (long long)e, ne[l]);
+    if (ne[l] > kMaxNe || nf[l] > kMaxNf)
+      return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_plan: element %lld n_e=%d n_f=%d exceeds %d/%d", (long long)e, ne[l], nf[l], kMaxNe, kMaxNf);
+    p.max_ne = std::max(p.max_ne, ne[l]);
+    p.max_nf = std::max(p.max_nf, nf[l]);
+  }
+
+  // ---- packed offsets --------------------------------------------------------------------------------------------
+  std::vector<std::vector<int64_t>> off(10, std::vector<int64_t>(n + 1, 0));
+  for (int64_t l = 0; l < n; ++l) {
+    const int64_t a = ne[l], f = nf[l];
+    const int64_t sz[10] = {a * a, a * f, f * a, f * f, a, f, f * f, f, a, factor_bytes((int)a)};
+    for (int k = 0; k < 10; ++k) off[k][l + 1] = off[k][l] + sz[k];
+  }
+  p.len.resize(10);
+  for (int k = 0; k < 10; ++k) p.len[k] = off[k][n];
+
+  // ---- buckets by (n_e, n_f), heaviest first ------------------------------------------------------------------
+  std::map<std::pair<int, int>, std::vector<int32_t>> bk;
+  for (int64_t l = 0; l < n; ++l) bk[{ne[l], nf[l]}].push_back((int32_t)l);
+  std::vector<std::pair<std::pair<int, int>, std::vector<int32_t>>> order(bk.begin(), bk.end());
+  std::sort(order.begin(), order.end(), [](const auto& x, const auto& y) {
+    const double wx = (double)x.first.first * x.first.first * (x.first.first + 3.0 * x.first.second) * x.second.size();
+    const double wy = (double)y.first.first * y.first.first * (y.first.first + 3.0 * y.first.second) * y.second.size();
+    return wx > wy;
+  });
+  int64_t scratch = 0;
+  for (auto& b : order) {
+    Bucket B;
+    B.ne = b.first.first;
+    B.nf = b.first.second;
+    B.count = (int64_t)b.second.size();
+    const Geo geo(B.ne, B.nf);
+    B.t_in_smem = geo.smem_bytes(true) <= (int64_t)ctx->smem_optin;
+    if (!B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
+    HDG_CUDA(ctx, upload(&B.d_elems, b.second.data(), b.second.size()));
+    p.buckets.push_back(B);
+  }
+  if (scratch > 0) {
+    if (cudaMalloc(&p.d_scratch, sizeof(double) * scratch) != cudaSuccess)
+      return fail(ctx, HDG_ERR_NOMEM, "hdg_plan: scratch of %lld doubles", (long long)scratch);
+    p.scratch_doubles = scratch;
+  }
+
+  // ---- owned skeleton rows ---------------------------------------------------------------------------------------
+  int64_t fmin = F, fmax = -1, cnt = 0;
+  for (int64_t f = 0; f < F; ++f) {
+    const int32_t l = m->face_elem[2 * f];
+    if (l >= eb && l < eb + n) { fmin = std::min(fmin, f); fmax = std::max(fmax, f); ++cnt; }
+  }
+  if (cnt == 0) { fmin = 0; fmax = -1; }
+  if (cnt != fmax - fmin + 1) return fail(ctx, HDG_ERR_ARG, "hdg_plan: owned faces are not a contiguous id range");
+  p.sk.f0 = fmin;
+  p.sk.f1 = fmax + 1;
+  p.sk.tr0 = face_off[p.sk.f0];
+  p.sk.ntr = face_off[p.sk.f1] - face_off[p.sk.f0];
+
+  // ---- uploads ----------------------------------------------------------------------------------------------------
+  HDG_CUDA(ctx, upload(&p.d_elem_face, m->elem_face, (size_t)(3 * E)));
+  HDG_CUDA(ctx, upload(&p.d_face_elem, m->face_elem, (size_t)(2 * F)));
+  HDG_CUDA(ctx, upload(&p.d_face_ndof, m->face_ndof, (size_t)F));
+  HDG_CUDA(ctx, upload(&p.d_face_off, face_off.data(), (size_t)(F + 1)));
+  HDG_CUDA(ctx, upload(&p.d_ne, ne.data(), (size_t)n));
+  HDG_CUDA(ctx, upload(&p.d_nf, nf.data(), (size_t)n));
+  for (int k = 0; k < 10; ++k) HDG_CUDA(ctx, upload(&p.d_off[k], off[k].data(), (size_t)(n + 1)));
+  HDG_CUDA(ctx, skeleton_symbolic(p, s));
+
+  // ---- exchange lists (faces shared between slabs) ----------------------------------------------------------------
+  const int R = ctx->nranks;
+  p.sk.send_counts.assign(R, 0); p.sk.send_displs.assign(R, 0);
+  p.sk.recv_counts.assign(R, 0); p.sk.recv_displs.assign(R, 0);
+  if (R > 1) {
+    auto rank_of = [&](int64_t e) {
+      return (int)(std::upper_bound(m->rank_elem_begin, m->rank_elem_begin + R + 1, e) - m->rank_elem_begin) - 1;
+    };
+    auto nf_of = [&](int64_t e) {
+      int t = 0;
+      for (int k = 0; k < 3; ++k) { const int32_t f = m->elem_face[3 * e + k]; if (f >= 0) t += m->face_ndof[f]; }
+      return t;
+    };
+    std::vector<std::tuple<int, int64_t, int64_t>> snd, rcv;   // (peer, face, element)
+    for (int64_t l = 0; l < n; ++l)
+      for (int k = 0; k < 3; ++k) {
+        const int32_t f = m->elem_face[3 * (eb + l) + k];
+        if (f < 0) continue;
+        const int32_t left = m->face_elem[2 * f];
+        if (left < eb || left >= eb + n) snd.emplace_back(rank_of(left), f, l);
+      }
+    for (int64_t f = p.sk.f0; f < p.sk.f1; ++f) {
+      const int32_t r = m->face_elem[2 * f + 1];
+      if (r >= 0 && (r < eb || r >= eb + n)) rcv.emplace_back(rank_of(r), f, r);
+    }
+    std::sort(snd.begin(), snd.end());
+    std::sort(rcv.begin(), rcv.end());
+    std::vector<int64_t> si, ri;
+    int64_t o = 0;
+    for (auto& t : snd) {
+      const int peer = std::get<0>(t);
+      const int64_t f = std::get<1>(t), l = std::get<2>(t);
+      const int64_t sz = (int64_t)m->face_ndof[f] * (1 + nf[l]);
+      si.insert(si.end(), {f, l, o});
+      p.sk.send_counts[peer] += sz;
+      o += sz;
+    }
+    p.sk.send_doubles = o;
+    o = 0;
+    for (auto& t : rcv) {
+      const int peer = std::get<0>(t);
+      const int64_t f = std::get<1>(t), e = std::get<2>(t);
+      const int64_t sz = (int64_t)m->face_ndof[f] * (1 + nf_of(e));
+      ri.insert(ri.end(), {f, e, o});
+      p.sk.recv_counts[peer] += sz;
+      o += sz;
+    }
+    p.sk.recv_doubles = o;
+    for (int r = 1; r < R; ++r) {
+      p.sk.send_displs[r] = p.sk.send_displs[r - 1] + p.sk.send_counts[r - 1];
+      p.sk.recv_displs[r] = p.sk.recv_displs[r - 1] + p.sk.recv_counts[r - 1];
+    }
+    p.sk.n_send_items = (int64_t)snd.size();
+    p.sk.n_recv_items = (int64_t)rcv.size();
+    HDG_CUDA(ctx, upload(&p.sk.d_send_items, si.data(), si.size()));
+    HDG_CUDA(ctx, upload(&p.sk.d_recv_items, ri.data(), ri.size()));
+  }
+
+  p.valid = true;
+  std::memset(info, 0, sizeof *info);
+  info->n_elem = n;
+  info->len_A = p.len[OFF_A]; info->len_B = p.len[OFF_B]; info->len_C = p.len[OFF_C]; info->len_D = p.len[OFF_D];
+  info->len_re = p.len[OFF_RE]; info->len_rf = p.len[OFF_RF];
+  info->len_S = p.len[OFF_S]; info->len_g = p.len[OFF_G]; info->len_u = p.len[OFF_U];
+  info->factor_bytes = p.len[OFF_F];
+  info->owned_face_begin = p.sk.f0; info->n_owned_faces = p.sk.f1 - p.sk.f0;
+  info->nnzb = p.sk.nnzb; info->nvals = p.sk.nvals;
+  info->owned_trace_begin = p.sk.tr0; info->n_owned_trace = p.sk.ntr;
+  info->n_trace = p.n_trace;
+  info->n_buckets = (int32_t)p.buckets.size();
+  info->max_ne = p.max_ne; info->max_nf = p.max_nf;
+  info->send_doubles = p.sk.send_doubles; info->recv_doubles = p.sk.recv_doubles;
+  return HDG_OK;
+}
+
+hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                        const double* r_e, const double* r_f, double* S, double* g, void* factors, int32_t* info,
+                        hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_condense: no plan");
+  ctx->launches = 0;
+  if (p.n == 0) return HDG_OK;
+  const void* ptrs[] = {A, B, C, D, r_e, r_f, S, g, factors, info};
+  for (const void* q : ptrs)
+    if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "hdg_condense: null or misaligned (16 B) pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  for (const Bucket& b : p.buckets) {
+    CondenseArgs a;
+    a.A = A; a.B = B; a.C = C; a.D = D; a.re = r_e; a.rf = r_f; a.S = S; a.g = g;
+    a.factors = static_cast<unsigned char*>(factors);
+    a.info = info;
+    a.elems = b.d_elems;
+    a.offA = p.d_off[OFF_A]; a.offB = p.d_off[OFF_B]; a.offC = p.d_off[OFF_C]; a.offD = p.d_off[OFF_D];
+    a.offRe = p.d_off[OFF_RE]; a.offRf = p.d_off[OFF_RF]; a.offS = p.d_off[OFF_S]; a.offG = p.d_off[OFF_G];
+    a.offF = p.d_off[OFF_F];
+    a.ne = b.ne; a.nf = b.nf; a.count = b.count;
+    a.scratch = p.d_scratch;
+    HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
+  }
+  return HDG_OK;
+}
+
+hdg_status hdg_assemble_skeleton(hdg_ctx ctx, const double* S, const double* g, int32_t* row_ptr, int32_t* col_idx,
+                                 int64_t* blk_off, double* K, double* E, double* send, hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_assemble_skeleton: no plan");
+  ctx->launches = 0;
+  if ((p.sk.nvals > 0 && !K) || (p.sk.ntr > 0 && !E) || (p.n > 0 && (!S || !g)))
+    return fail(ctx, HDG_ERR_ARG, "hdg_assemble_skeleton: null pointer");
+  if (p.sk.send_doubles > 0 && !send) return fail(ctx, HDG_ERR_ARG, "hdg_assemble_skeleton: send buffer required");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int64_t nrows = p.sk.f1 - p.sk.f0;
+  if (row_ptr) HDG_CUDA(ctx, cudaMemcpyAsync(row_ptr, p.sk.d_row_ptr, sizeof(int32_t) * (nrows + 1), cudaMemcpyDeviceToDevice, s));
+  if (col_idx && p.sk.nnzb) HDG_CUDA(ctx, cudaMemcpyAsync(col_idx, p.sk.d_col_idx, sizeof(int32_t) * p.sk.nnzb, cudaMemcpyDeviceToDevice, s));
+  if (blk_off) HDG_CUDA(ctx, cudaMemcpyAsync(blk_off, p.sk.d_blk_off, sizeof(int64_t) * (p.sk.nnzb + 1), cudaMemcpyDeviceToDevice, s));
+  HDG_CUDA(ctx, launch_assemble(p, S, g, K, E, send, s, &ctx->launches));
+  return HDG_OK;
+}
+
+hdg_status hdg_exchange_counts(hdg_ctx ctx, int64_t* send_counts, int64_t* send_displs, int64_t* recv_counts,
+                               int64_t* recv_displs) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_exchange_counts: no plan");
+  for (int r = 0; r < ctx->nranks; ++r) {
+    if (send_counts) send_counts[r] = p.sk.send_counts[r];
+    if (send_displs) send_displs[r] = p.sk.send_displs[r];
+    if (recv_counts) recv_counts[r] = p.sk.recv_counts[r];
+    if (recv_displs) recv_displs[r] = p.sk.recv_displs[r];
+  }
+  return HDG_OK;
+}
+
+hdg_status hdg_skeleton_accumulate(hdg_ctx ctx, const double* recv, double* K, double* E, hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_skeleton_accumulate: no plan");
+  if (p.sk.recv_doubles > 0 && (!recv || !K || !E)) return fail(ctx, HDG_ERR_ARG, "hdg_skeleton_accumulate: null pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  HDG_CUDA(ctx, launch_accumulate(p, recv, K, E, s, &ctx->launches));
+  return HDG_OK;
+}
+
+hdg_status hdg_backsubstitute(hdg_ctx ctx, const void* factors, const double* B, const double* r_e, const double* lambda,
+                              double* u, hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_backsubstitute: no plan");
+  ctx->launches = 0;
+  if (p.n == 0) return HDG_OK;
+  const void* ptrs[] = {factors, B, r_e, u};
+  for (const void* q : ptrs)
+    if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "hdg_backsubstitute: null or misaligned (16 B) pointer");
+  if (!lambda && p.n_trace > 0) return fail(ctx, HDG_ERR_ARG, "hdg_backsubstitute: null lambda");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  for (const Bucket& b : p.buckets) {
+    BacksubArgs a;
+    a.factors = static_cast<const unsigned char*>(factors);
+    a.B = B; a.re = r_e; a.lambda = lambda; a.u = u;
+    a.elems = b.d_elems;
+    a.offB = p.d_off[OFF_B]; a.offRe = p.d_off[OFF_RE]; a.offU = p.d_off[OFF_U]; a.offF = p.d_off[OFF_F];
+    a.elem_face = p.d_elem_face; a.face_ndof = p.d_face_ndof; a.face_off = p.d_face_off;
+    a.elem_begin = p.eb;
+    a.ne = b.ne; a.nf = b.nf; a.count = b.count;
+    HDG_CUDA(ctx, launch_backsub(a, ctx->sms, s, &ctx->launches));
+  }
+  return HDG_OK;
+}
+
+hdg_status hdg_first_error(hdg_ctx ctx, const int32_t* info, int64_t* elem, int32_t* code, hdg_stream stream) {
+  if (!ctx || !elem || !code) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_first_error: no plan");
+  *elem = -1;
+  *code = 0;
+  if (p.n == 0) return HDG_OK;
+  if (!info) return fail(ctx, HDG_ERR_ARG, "hdg_first_error: null info");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  int64_t* d = nullptr;
+  HDG_CUDA(ctx, cudaMalloc(&d, sizeof(int64_t)));
+  int64_t h = INT64_MAX;
+  cudaError_t e = launch_first_error(info, p.n, d, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "hdg_first_error");
+  if (h == INT64_MAX) return HDG_OK;
+  *elem = h;
+  if (cudaMemcpy(code, info + h, sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(ctx, HDG_ERR_CUDA, "hdg_first_error: copy");
+  return fail(ctx, HDG_ERR_SINGULAR, "singular local block: element %lld (info %d)", (long long)(p.eb + h), *code);
+}
+
+}  // extern "C"

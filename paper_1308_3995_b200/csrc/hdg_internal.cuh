@@ -1,0 +1,133 @@
+// hdg_internal.cuh — shared definitions of libhdg's kernels and host runtime (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hdg.h"
+
+namespace hdg {
+
+constexpr int kNB = 16;          // panel width of the blocked elimination (multiple of 4 = DMMA k)
+constexpr int kMaxNe = 256;      // largest n_e handled by the condensation / back-substitution kernels
+constexpr int kMaxNf = 96;       // largest element trace size n_f
+constexpr int kMaxCT = (kMaxNf + 1 + 7) / 8;   // column tiles of [S | g] in phase B
+
+__host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Geometry of the per-element working matrix T = [A | pad | B | r_e | pad] (rows padded to R8 with zeros).
+// Columns: A at [0, ne), B at [CB, CB+nf), r_e at CB+nf, zero padding up to C8; row stride ldT = 4 mod 16
+// doubles so that DMMA A-, B- and C-fragment accesses are shared-memory bank-conflict free.
+struct Geo {
+  int ne, nf, R8, CB, NC, C8, ldT, ldP;
+  __host__ __device__ Geo(int ne_, int nf_) : ne(ne_), nf(nf_) {
+    R8 = round_up(ne, 8);
+    CB = R8;
+    NC = CB + nf + 1;
+    C8 = round_up(NC, 8);
+    ldT = round_up(C8 - 4, 16) + 4;
+    ldP = R8 + 1;
+  }
+  __host__ __device__ int64_t t_doubles() const { return (int64_t)R8 * ldT; }
+  // shared memory of the condensation kernel: [T (if in smem)] [P: panel, col-major] [rcp] [piv] [flag]
+  __host__ __device__ int64_t smem_bytes(bool t_in_smem) const {
+    return 8 * ((t_in_smem ? t_doubles() : 0) + (int64_t)kNB * ldP + R8) + 4 * (int64_t)R8 + 16;
+  }
+};
+
+// Opaque per-element factor record: [LU of P A_e, column-major, ne*ne doubles][perm: ne int32][pad to 16 B].
+__host__ __device__ inline int64_t factor_bytes(int ne) { return ((int64_t)ne * ne * 8 + (int64_t)ne * 4 + 15) / 16 * 16; }
+
+struct CondenseArgs {
+  const double *A, *B, *C, *D, *re, *rf;
+  double *S, *g;
+  unsigned char* factors;
+  int32_t* info;
+  const int32_t* elems;   // local element ids of this bucket
+  const int64_t *offA, *offB, *offC, *offD, *offRe, *offRf, *offS, *offG, *offF;
+  int ne, nf;
+  int64_t count;
+  double* scratch;        // global workspace for T when it does not fit in shared memory
+};
+
+struct BacksubArgs {
+  const unsigned char* factors;
+  const double *B, *re, *lambda;
+  double* u;
+  const int32_t* elems;
+  const int64_t *offB, *offRe, *offU, *offF;
+  const int32_t* elem_face;   // global [E][3]
+  const int32_t* face_ndof;   // global [F]
+  const int64_t* face_off;    // global [F+1]
+  int64_t elem_begin;
+  int ne, nf;
+  int64_t count;
+};
+
+struct Bucket {
+  int ne, nf;
+  int64_t count;
+  int32_t* d_elems;   // device list of local element ids
+  bool t_in_smem;
+};
+
+// Skeleton assembly data (owned rows).
+struct Skeleton {
+  int64_t f0 = 0, f1 = 0;          // owned face range
+  int64_t nnzb = 0, nvals = 0;
+  int64_t tr0 = 0, ntr = 0;         // owned trace dof range
+  int32_t* d_row_ptr = nullptr;     // [nrows+1]
+  int32_t* d_col_idx = nullptr;     // [nnzb]
+  int64_t* d_blk_off = nullptr;     // [nnzb+1]
+  int32_t* d_blk_row = nullptr;     // [nnzb] face id of the block's row
+  // exchange (nranks > 1)
+  std::vector<int64_t> send_counts, send_displs, recv_counts, recv_displs;
+  int64_t send_doubles = 0, recv_doubles = 0;
+  int64_t n_send_items = 0, n_recv_items = 0;
+  int64_t* d_send_items = nullptr;  // [n][3]: face, local element, offset (doubles) in send buffer
+  int64_t* d_recv_items = nullptr;  // [n][3]: face, global element, offset in recv buffer
+};
+
+struct Plan {
+  bool valid = false;
+  int64_t E = 0, F = 0, eb = 0, n = 0;
+  int32_t *d_elem_face = nullptr, *d_face_elem = nullptr, *d_face_ndof = nullptr;
+  int64_t* d_face_off = nullptr;
+  int32_t *d_ne = nullptr, *d_nf = nullptr;   // local elements
+  int64_t* d_off[10] = {};                     // A B C D re rf S g u F(bytes): [n+1] each
+  std::vector<int64_t> len;                    // totals of the above
+  std::vector<Bucket> buckets;
+  Skeleton sk;
+  double* d_scratch = nullptr;
+  int64_t scratch_doubles = 0;
+  int max_ne = 0, max_nf = 0;
+  int64_t n_trace = 0;
+};
+
+enum { OFF_A = 0, OFF_B, OFF_C, OFF_D, OFF_RE, OFF_RF, OFF_S, OFF_G, OFF_U, OFF_F };
+
+}  // namespace hdg
+
+struct hdg_ctx_s {
+  int device = 0, rank = 0, nranks = 1;
+  int sms = 148;
+  size_t smem_optin = 0;
+  std::string last_error;
+  hdg::Plan plan;
+  int64_t launches = 0;
+};
+
+// kernel launchers (defined in the .cu files); return cudaError_t of the launch
+namespace hdg {
+cudaError_t launch_condense(const CondenseArgs& a, bool t_in_smem, int sms, cudaStream_t s, int64_t* launches);
+cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_t* launches);
+cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s);
+cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, double* K, double* E, double* send,
+                            cudaStream_t s, int64_t* launches);
+cudaError_t launch_accumulate(const Plan& p, const double* recv, double* K, double* E, cudaStream_t s,
+                              int64_t* launches);
+cudaError_t launch_first_error(const int32_t* info, int64_t n, int64_t* d_out, cudaStream_t s);
+}  // namespace hdg

@@ -1,0 +1,56 @@
+"""The C-ABI library loads and exports every symbol include/hdg.h declares (CPU-only: no compute calls)."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "hdg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hdg_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ("hdg_condense", "hdg_assemble_skeleton", "hdg_backsubstitute", "hdg_plan", "hdg_ctx_create"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1308_3995_b200 import build as b
+    so = b.build()
+    lib = ctypes.CDLL(so)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    import paper_1308_3995_b200 as hdg
+    assert set(hdg.EXPORTED) == set(declared_functions())
+    L = hdg.lib()
+    assert L.hdg_version().decode().startswith("libhdg")
+    assert L.hdg_max_elem_ndof() >= 252 and L.hdg_max_face_ndof() >= 72      # C5: p = 5, n_f up to 72
+    assert L.hdg_status_string(0).decode() == "ok"
+
+
+def test_sm100a_code_in_library():
+    import shutil
+    import subprocess
+    from paper_1308_3995_b200 import build as b
+    so = b.build()
+    if not shutil.which("cuobjdump"):
+        return
+    out = subprocess.run(["cuobjdump", "-lelf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    assert "DMMA" in sass          # FP64 tensor-core tiles in the Schur / trailing updates
+
+
+def test_product_has_no_oracle_dependency():
+    """The product path must not import, link or execute anything under oracle/ (nor gen/)."""
+    pkg = os.path.join(ROOT, "paper_1308_3995_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f
+                assert "import gen" not in txt and "philox_normal.h" not in txt, f
