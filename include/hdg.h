@@ -152,6 +152,10 @@ hdg_status hdg_first_error(hdg_ctx ctx, const int32_t* info, int64_t* elem, int3
  * calls of this context (instrumentation for the benchmark's launch count). */
 int64_t hdg_launch_count(hdg_ctx ctx);
 
+/* Instrumentation (profiling builds/tools only): when non-NULL, hdg_condense records clock64() stamps of CTA 0
+ * into the device buffer trace (>= 4 x 256 int64), see tools/trace_condense.py. NULL (default) = off. */
+hdg_status hdg_debug_set_trace(hdg_ctx ctx, long long* trace);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,8 @@ def lib():
         L.hdg_first_error.argtypes = [P, P, ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_int32), P]
         L.hdg_launch_count.restype = I64
         L.hdg_launch_count.argtypes = [P]
+        L.hdg_debug_set_trace.restype = I32
+        L.hdg_debug_set_trace.argtypes = [P, P]
         L.hdg_max_elem_ndof.restype = I32
         L.hdg_max_face_ndof.restype = I32
         _lib = L
@@ -91,7 +93,7 @@ def lib():
 EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status_string", "hdg_ctx_create",
             "hdg_ctx_destroy", "hdg_last_error", "hdg_plan", "hdg_condense", "hdg_assemble_skeleton",
             "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
-            "hdg_launch_count")
+            "hdg_launch_count", "hdg_debug_set_trace")
 
 
 def _ptr(t):
@@ -254,6 +256,10 @@ class Context:
         if st not in (HDG_OK, HDG_ERR_SINGULAR):
             self._check(st, "hdg_first_error")
         return e.value, c.value
+
+    def debug_set_trace(self, buf):
+        """Instrumentation: record clock64 stamps of CTA 0 into the int64 CUDA tensor buf (None = off)."""
+        self._check(self._L.hdg_debug_set_trace(self._h, _ptr(buf)), "hdg_debug_set_trace")
 
     def launch_count(self) -> int:
         return int(self._L.hdg_launch_count(self._h))

@@ -109,6 +109,12 @@ const char* hdg_last_error(hdg_ctx ctx) { return ctx ? ctx->last_error.c_str() :
 
 int64_t hdg_launch_count(hdg_ctx ctx) { return ctx ? ctx->launches : 0; }
 
+hdg_status hdg_debug_set_trace(hdg_ctx ctx, long long* trace) {
+  if (!ctx) return HDG_ERR_ARG;
+  ctx->trace = trace;
+  return HDG_OK;
+}
+
 hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_stream stream) {
   if (!ctx) return HDG_ERR_ARG;
   if (!m || !info || !m->elem_face || !m->face_elem || !m->face_ndof || !m->elem_ndof)
@@ -322,6 +328,7 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
     a.offF = p.d_off[OFF_F];
     a.ne = b.ne; a.nf = b.nf; a.count = b.count;
     a.scratch = p.d_scratch;
+    a.trace = ctx->trace;
     HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
   }
   return HDG_OK;

@@ -2,27 +2,45 @@
 //
 // For each element e (Eq. hybridsystem; "condense"):
 //     S_e = D_e - C_e A_e^-1 B_e,   g_e = r_f - C_e A_e^-1 r_e,
-// with A_e factored by Gaussian elimination with partial pivoting and the factorization kept for
-// the reconstruction.
+// with A_e factored by Gaussian elimination with partial pivoting (GEPP) and the factorization
+// kept for the reconstruction.
 //
-// One CTA owns one element at a time (persistent grid). The working matrix T = [A_e | B_e | r_e] lives in
-// shared memory (or an L2-resident global scratch slab when it does not fit, hp degrees p >= 4):
-//   phase A  : blocked right-looking LU with partial pivoting on the A rows, carried across the B|r columns
-//              (T <- [L\U | L^-1 P B | L^-1 P r_e]). Per panel of kNB columns: warp 0 factors the panel
-//              (pivot search with warp shuffles, first index on ties like the oracle), all threads apply the
-//              row interchanges and the unit-lower triangular solve for U12, then the trailing update
-//              T22 -= L21 U12 runs on the FP64 tensor cores (DMMA m8n8k4, operands from shared memory).
-//   factors  : L\U written column-major + the row permutation, for the back-substitution kernel.
-//   phase A' : blocked backward substitution X = U^-1 [L^-1 P B | L^-1 P r_e] = A_e^-1 [B_e | r_e], in place,
-//              trailing updates again on DMMA.
-//   phase B  : [S_e | g_e] = [D_e | r_f] - C_e X as one DMMA GEMM per element (n_f x (n_f+1) x n_e), C_e and
-//              D_e streamed from HBM straight into the fragments, results stored straight to HBM.
-// The flop count equals SURVEY.md §8(d)'s algorithmic count n_e(n_e-1)(4n_e+1)/6 + (n_f+1)(2n_e^2-n_e)
-// + 2 n_f n_e (n_f+1) up to O(n_e^2) terms.
+// One CTA owns one element at a time (persistent grid). The working matrix T = [A_e | 0 | B_e | r_e | 0]
+// (rows padded with zeros to a multiple of 16) lives in shared memory, or in an L2-resident global scratch slab
+// when it does not fit (hp degrees p >= 4).
+//
+//   phase A  : blocked right-looking elimination of the A rows across all columns, panels of kNB = 16:
+//              T <- [L\U | L^-1 P B | L^-1 P r_e].
+//              Fast path (speculative GEPP): the 16x16 diagonal block is factored by one warp in natural order
+//              and inverted (L11^-1, U11^-1); L21 = A21 U11^-1, U12 = L11^-1 A12 and the trailing update
+//              A22 -= L21 U12 all run on the FP64 tensor cores (DMMA m8n8k4). Every multiplier is checked:
+//              if any |l_ik| > 1 (or a pivot is 0), partial pivoting would have interchanged rows, and the
+//              element is re-staged and redone on the pivoting path. When the check passes, the pivot sequence
+//              of GEPP is the identity and this IS GEPP.
+//              Pivoting path: one warp factors the whole panel column by column with the GEPP pivot search
+//              (maximal |a_ik|, lowest index on ties), interchanges are applied to the
+//              other columns, then U12 and the trailing update as above.
+//   factors  : L\U written column-major + the row permutation (for hdg_backsubstitute).
+//   phase A' : X = U^-1 [L^-1 P B | L^-1 P r_e] = A_e^-1 [B_e | r_e] by blocked backward substitution, panels
+//              bottom-up: X_p = U_pp^-1 W_p and W_<p -= U_<p,p X_p, both DMMA.
+//   phase B  : [S_e | g_e] = [D_e | r_f] - C_e X, DMMA GEMM n_f x (n_f+1) x n_e per element; C_e, D_e read from
+//              HBM straight into fragments, S_e, g_e stored straight to HBM.
+// FLOPs: SURVEY.md §8(d)'s algorithmic count n_e(n_e-1)(4n_e+1)/6 + (n_f+1)(2n_e^2-n_e) + 2 n_f n_e (n_f+1)
+// plus the O(16 n_e^2) explicit 16x16 inverse applications.
 #include "hdg_internal.cuh"
 
 namespace hdg {
 namespace {
+
+constexpr int NB = kNB;   // 16
+
+// instrumentation: stamp k of element-iteration `it` (CTA 0, first 4 elements), per warp 0 / warp 1
+#define HDG_STAMP(trace, it, k)                                                                          \
+  do {                                                                                                   \
+    if ((trace) && blockIdx.x == 0 && (it) < 4 && (threadIdx.x == 0 || threadIdx.x == 32))               \
+      (trace)[(it) * 256 + (threadIdx.x >> 5) * 128 + (k)] = clock64();                                  \
+  } while (0)
+constexpr int LDI = 20;   // row stride of the 16x16 inverse buffers (= 4 mod 16: conflict-free fragments)
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -30,17 +48,18 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// dst[r][c] -= sum_{k < nb} As[r][k] * Bs[k][c] over row tiles [r_lo, r_hi) and column tiles [c_lo, c_hi)
-// (all multiples of 8; nb multiple of 4). dst, As, Bs share the row stride ld. Work unit: a 2x2 block of 8x8
-// tiles per warp, so every A/B fragment loaded from shared memory feeds two DMMAs.
-template <int NWARPS>
+// dst[r][c] -= sum_{k < nk} As[r][k] * Bs[k][c] over rows [r_lo, r_hi) and columns [c_lo, c_hi) (multiples of 8;
+// nk multiple of 4). dst, As, Bs share the row stride ld. Work unit: a 2x2 block of 8x8 tiles per warp.
+// Blocks are numbered row-major over the 16x16 grid; this warp takes blocks first, first + stride, ...
 __device__ __forceinline__ void mma_update(double* dst, const double* As, const double* Bs, int ld, int r_lo, int r_hi,
-                                           int c_lo, int c_hi, int nb, int warp, int lane) {
+                                           int c_lo, int c_hi, int nk, int first, int stride, int lane,
+                                           int max_blocks = 1 << 30) {
   const int RT = (r_hi - r_lo) >> 3, CT = (c_hi - c_lo) >> 3;
   if (RT <= 0 || CT <= 0) return;
   const int BR = (RT + 1) >> 1, BC = (CT + 1) >> 1;
+  const int nblk = min(BR * BC, max_blocks);
   const int gid = lane >> 2, tig = lane & 3;
-  for (int blk = warp; blk < BR * BC; blk += NWARPS) {
+  for (int blk = first; blk < nblk; blk += stride) {
     const int br = blk / BC, bc = blk - br * BC;
     const int r0 = r_lo + br * 16, c0 = c_lo + bc * 16;
     const bool two_r = (br * 2 + 1) < RT, two_c = (bc * 2 + 1) < CT;
@@ -49,16 +68,15 @@ __device__ __forceinline__ void mma_update(double* dst, const double* As, const 
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
+        acc[i][j][0] = 0.0;
+        acc[i][j][1] = 0.0;
         if ((i == 0 || two_r) && (j == 0 || two_c)) {
           const double2 v = *reinterpret_cast<const double2*>(dst + (r0 + 8 * i + gid) * ld + c0 + 8 * j + 2 * tig);
           acc[i][j][0] = v.x;
           acc[i][j][1] = v.y;
-        } else {
-          acc[i][j][0] = 0.0;
-          acc[i][j][1] = 0.0;
         }
       }
-    for (int k = 0; k < nb; k += 4) {
+    for (int k = 0; k < nk; k += 4) {
       const double a0 = -As[(r0 + gid) * ld + k + tig];
       const double a1 = two_r ? -As[(r0 + 8 + gid) * ld + k + tig] : 0.0;
       const double b0 = Bs[(k + tig) * ld + c0 + gid];
@@ -78,23 +96,208 @@ __device__ __forceinline__ void mma_update(double* dst, const double* As, const 
   }
 }
 
-// Panel factorization by one warp: rows [jb, ne), columns [jb, jb+nb) of T, staged column-major in P.
-// Partial pivoting: |pivot| maximal over rows k..ne-1 of the current column, first (lowest) index on ties
-// (SURVEY.md §8(c) O1). Records piv[k] (absolute row) and rcp[k] = 1 / pivot; sets *flag = k+1 at the first
-// exactly-zero pivot.
-__device__ __forceinline__ void panel_factor(double* T, int ldT, double* P, int ldP, int jb, int nb, int ne, int* piv,
-                                             double* rcp, int* flag, int lane) {
-  const int rows = ne - jb;
-  for (int idx = lane; idx < rows * kNB; idx += 32) {
-    const int r = idx / kNB, c = idx - r * kNB;
-    if (c < nb) P[c * ldP + r] = T[(jb + r) * ldT + jb + c];
+// 1/x with one MUFU.RCP64H and two Newton steps (no slow path; pivots here are finite and non-zero, a zero or
+// non-finite pivot is caught by the GEPP speculation check and redone on the pivoting path).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;\n" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Fast path: factor the nb x nb diagonal block at (jb, jb) in natural row order and invert both factors, one
+// warp, laid out by COLUMNS: lane j < 16 holds column j of D, lane 16 + j column j of the identity. Step c: lane
+// c forms the multipliers of column c and publishes them in `buf` (shared memory broadcast); every trailing D
+// column and every identity column applies the row operations, so the forward pass maps [D | I] to
+// [L\U | L^-1]. U^-1 then comes from a backward substitution of the identity columns against U (read from T).
+// FULL: nb == 16 (compile-time trip counts, no bounds checks). Linv/Uinv: row-major 16x16, stride LDI, zero
+// padded beyond nb. Returns true if GEPP would have interchanged rows (|a_ik| > |a_kk|, i > k) or a pivot is 0.
+template <bool FULL>
+__device__ __forceinline__ bool diag_factor_t(double* T, int ldT, int jb, int nb_in, double* Linv, double* Uinv,
+                                              double* buf, int lane) {
+  const int nb = FULL ? NB : nb_in;
+  const int j = lane & 15;
+  const bool dl = lane < 16;
+  const bool valid = j < nb;
+  double* Dg = T + jb * ldT + jb;
+  double x[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const bool in = FULL || (valid && i < nb);
+    x[i] = dl ? (in ? Dg[i * ldT + j] : 0.0) : ((i == j) ? 1.0 : 0.0);
+  }
+  bool viol = false;
+  // reciprocal of the pivot of step 0 (lane 0); later pivots' reciprocals are formed right after their final
+  // update in the previous step, overlapping the rest of that step's row operations
+  double rnext = fast_rcp(x[0]);
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    if (!FULL && c >= nb) break;
+    double* bc = buf + (c & 1) * 16;             // double-buffered broadcast slot
+    if (lane == c) {
+      const double pv = x[c];
+      viol |= !(fabs(pv) > 0.0);
+#pragma unroll
+      for (int i = c + 1; i < NB; ++i) {
+        viol |= fabs(x[i]) > fabs(pv);
+        const double m = x[i] * rnext;
+        x[i] = m;
+        bc[i] = m;
+      }
+    }
+    __syncwarp();
+    const double xc = x[c];
+    if (!dl || j > c) {
+      if (c + 1 < NB) {
+        x[c + 1] = fma(-bc[c + 1], xc, x[c + 1]);
+        rnext = fast_rcp(x[c + 1]);              // used by lane c+1 in step c+1
+      }
+#pragma unroll
+      for (int i = c + 2; i < NB; ++i) x[i] = fma(-bc[i], xc, x[i]);
+    }
+  }
+  if (dl) {
+    if (FULL || valid) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (FULL || i < nb) Dg[i * ldT + j] = x[i];
+      buf[32 + j] = fast_rcp(x[j]);          // 1 / u_jj
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) Linv[i * LDI + j] = (FULL || (valid && i < nb)) ? x[i] : 0.0;
   }
   __syncwarp();
+  // U^-1: column j solves U y = e_j (identity lanes), U read back from T (broadcast loads)
+  if (!dl) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) x[i] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int c = NB - 1; c >= 0; --c) {
+      if (FULL || c < nb) {
+        x[c] *= buf[32 + c];
+#pragma unroll
+        for (int i = 0; i < c; ++i) x[i] = fma(-Dg[i * ldT + c], x[c], x[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) Uinv[i * LDI + j] = (FULL || (valid && i < nb)) ? x[i] : 0.0;
+  }
+  return __any_sync(0xffffffffu, viol);
+}
+
+__device__ __forceinline__ bool diag_factor(double* T, int ldT, int jb, int nb, double* Linv, double* Uinv,
+                                            double* buf, int lane) {
+  return nb == NB ? diag_factor_t<true>(T, ldT, jb, nb, Linv, Uinv, buf, lane)
+                  : diag_factor_t<false>(T, ldT, jb, nb, Linv, Uinv, buf, lane);
+}
+
+// Pivoting path: inverses of the factored diagonal block already in T (L11\U11 at (jb, jb)), same registers
+// scheme as diag_factor without the elimination.
+__device__ __forceinline__ void diag_inverses(const double* T, int ldT, int jb, int nb, double* Linv, double* Uinv,
+                                              int lane) {
+  double d[NB], e[NB], rc[NB];
+  const bool mine = lane < nb;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) d[j] = mine ? T[(jb + lane) * ldT + jb + j] : 0.0;
+#pragma unroll
+  for (int c = 0; c < NB; ++c) rc[c] = c < nb ? 1.0 / T[(jb + c) * ldT + jb + c] : 0.0;
+  // L^-1 by forward substitution on [L | I] (unit diagonal)
+#pragma unroll
+  for (int j = 0; j < NB; ++j) e[j] = (j == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    if (c < nb) {
+      double perow[NB];
+#pragma unroll
+      for (int j = 0; j <= c; ++j) perow[j] = __shfl_sync(0xffffffffu, e[j], c);
+      if (lane > c && mine) {
+        const double l = d[c];
+#pragma unroll
+        for (int j = 0; j <= c; ++j) e[j] = fma(-l, perow[j], e[j]);
+      }
+    }
+  }
+  if (lane < NB) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) Linv[lane * LDI + j] = mine ? e[j] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) e[j] = (j == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int c = NB - 1; c >= 0; --c) {
+    if (c < nb) {
+      if (lane == c) {
+#pragma unroll
+        for (int j = c; j < NB; ++j) e[j] *= rc[c];
+      }
+      double pf[NB];
+#pragma unroll
+      for (int j = c; j < NB; ++j) pf[j] = __shfl_sync(0xffffffffu, e[j], c);
+      if (lane < c) {
+        const double u = d[c];
+#pragma unroll
+        for (int j = c; j < NB; ++j) e[j] = fma(-u, pf[j], e[j]);
+      }
+    }
+  }
+  if (lane < NB) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) Uinv[lane * LDI + j] = mine ? e[j] : 0.0;
+  }
+}
+
+// T[jb..jb+16, c0..c0+8) <- Inv (16x16) * T[jb..jb+16, c0..c0+8), in place; one warp, one column tile.
+__device__ __forceinline__ void inv_times_tile(double* T, int ldT, int jb, const double* Inv, int c0, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  double b[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) b[kk] = T[(jb + 4 * kk + tig) * ldT + c0 + gid];
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    dmma(acc[0], Inv[gid * LDI + 4 * kk + tig], b[kk]);
+    dmma(acc[1], Inv[(8 + gid) * LDI + 4 * kk + tig], b[kk]);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+    *reinterpret_cast<double2*>(T + (jb + 8 * i + gid) * ldT + c0 + 2 * tig) = make_double2(acc[i][0], acc[i][1]);
+}
+
+// T[r0..r0+8, jb..jb+16) <- T[r0..r0+8, jb..jb+16) * Uinv, in place (L21 = A21 U11^-1); one warp, one row tile.
+// Returns whether any multiplier exceeds 1 in magnitude (GEPP would have pivoted).
+__device__ __forceinline__ bool tile_times_uinv(double* T, int ldT, int jb, const double* Uinv, int r0, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  double a[4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) a[kk] = T[(r0 + gid) * ldT + jb + 4 * kk + tig];
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    dmma(acc[0], a[kk], Uinv[(4 * kk + tig) * LDI + gid]);
+    dmma(acc[1], a[kk], Uinv[(4 * kk + tig) * LDI + 8 + gid]);
+  }
+  bool viol = false;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    viol |= fabs(acc[j][0]) > 1.0 || fabs(acc[j][1]) > 1.0;
+    *reinterpret_cast<double2*>(T + (r0 + gid) * ldT + jb + 8 * j + 2 * tig) = make_double2(acc[j][0], acc[j][1]);
+  }
+  return viol;
+}
+
+// Pivoting-path panel factorization (GEPP) by one warp directly in T: rows [jb, ne), columns [jb, jb+nb).
+// Records piv[k] (absolute row); sets *flag = k+1 at the first exactly-zero pivot.
+__device__ __forceinline__ void panel_factor_pivot(double* T, int ldT, int jb, int nb, int ne, int* piv, int* flag,
+                                                   int lane) {
   for (int c = 0; c < nb; ++c) {
+    const int k = jb + c;
     double best = -1.0;
     int bi = 0x7fffffff;
-    for (int r = c + lane; r < rows; r += 32) {
-      const double v = fabs(P[c * ldP + r]);
+    for (int r = k + lane; r < ne; r += 32) {
+      const double v = fabs(T[r * ldT + k]);
       if (v > best) { best = v; bi = r; }
     }
 #pragma unroll
@@ -103,78 +306,82 @@ __device__ __forceinline__ void panel_factor(double* T, int ldT, double* P, int 
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
       if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
     }
-    const int pr = bi < rows ? bi : c;   // all-NaN column (after a zero pivot): keep the row, stay in range
-    if (pr != c && lane < nb) {
-      const double t = P[lane * ldP + c];
-      P[lane * ldP + c] = P[lane * ldP + pr];
-      P[lane * ldP + pr] = t;
+    const int pr = bi < ne ? bi : k;   // all-NaN column (after a zero pivot): keep the row
+    if (pr != k && lane < nb) {
+      const double t = T[k * ldT + jb + lane];
+      T[k * ldT + jb + lane] = T[pr * ldT + jb + lane];
+      T[pr * ldT + jb + lane] = t;
     }
     __syncwarp();
-    const double pv = P[c * ldP + c];
+    const double pv = T[k * ldT + k];
     const double rp = 1.0 / pv;
     if (lane == 0) {
-      piv[jb + c] = jb + pr;
-      rcp[jb + c] = rp;
-      if (pv == 0.0 && *flag == 0) *flag = jb + c + 1;
+      piv[k] = pr;
+      if (pv == 0.0 && *flag == 0) *flag = k + 1;
     }
-    for (int r = c + 1 + lane; r < rows; r += 32) {
-      const double l = P[c * ldP + r] * rp;
-      P[c * ldP + r] = l;
-      for (int c2 = c + 1; c2 < nb; ++c2) P[c2 * ldP + r] -= l * P[c2 * ldP + c];
+    for (int r = k + 1 + lane; r < ne; r += 32) {
+      const double l = T[r * ldT + k] * rp;
+      T[r * ldT + k] = l;
+      for (int c2 = c + 1; c2 < nb; ++c2) T[r * ldT + jb + c2] = fma(-l, T[k * ldT + jb + c2], T[r * ldT + jb + c2]);
     }
     __syncwarp();
-  }
-  for (int idx = lane; idx < rows * kNB; idx += 32) {
-    const int r = idx / kNB, c = idx - r * kNB;
-    if (c < nb) T[(jb + r) * ldT + jb + c] = P[c * ldP + r];
   }
 }
 
-template <int THREADS, bool T_SMEM>
-__global__ void __launch_bounds__(THREADS) condense_kernel(const CondenseArgs a) {
-  constexpr int NWARPS = THREADS / 32;
-  extern __shared__ __align__(16) double smem[];
-  const Geo geo(a.ne, a.nf);
-  const int ne = geo.ne, nf = geo.nf, R8 = geo.R8, CB = geo.CB, C8 = geo.C8, ldT = geo.ldT, ldP = geo.ldP;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* T = T_SMEM ? smem : a.scratch + (int64_t)blockIdx.x * geo.t_doubles();
-  double* P = T_SMEM ? smem + geo.t_doubles() : smem;
-  double* rcp = P + kNB * ldP;
-  int* piv = reinterpret_cast<int*>(rcp + R8);
-  int* flag = piv + R8;
-  const int npan = (ne + kNB - 1) / kNB;
+// ---- a1 staging with the Tensor Memory Accelerator: bulk row copies global -> shared, completion counted on an
+//      mbarrier (transaction bytes), so the next element streams in while the current one computes --------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-  for (int64_t it = blockIdx.x; it < a.count; it += gridDim.x) {
-    const int64_t l = a.elems ? a.elems[it] : it;
-    const double* A = a.A + a.offA[l];
-    const double* Bm = a.B + a.offB[l];
-    const double* re = a.re + a.offRe[l];
-
-    // ---- a1 stage: T = [A | 0 | B | r_e | 0], zero rows [ne, R8) -------------------------------------------
-    for (int i = warp; i < R8; i += NWARPS) {
-      double* Ti = T + i * ldT;
-      if (i < ne) {
-        const double2* Ai = reinterpret_cast<const double2*>(A + (int64_t)i * ne);
-        for (int j = lane; j < ne / 2; j += 32) reinterpret_cast<double2*>(Ti)[j] = __ldg(Ai + j);
-        for (int j = ne + lane; j < CB; j += 32) Ti[j] = 0.0;
-        const double2* Bi = reinterpret_cast<const double2*>(Bm + (int64_t)i * nf);
-        for (int j = lane; j < nf / 2; j += 32) reinterpret_cast<double2*>(Ti + CB)[j] = __ldg(Bi + j);
-        if (lane == 0) Ti[CB + nf] = __ldg(re + i);
-        for (int j = CB + nf + 1 + lane; j < C8; j += 32) Ti[j] = 0.0;
-      } else {
-        for (int j = lane; j < C8; j += 32) Ti[j] = 0.0;
-      }
+// Phase A. PIVOT = false: speculative natural-order pass with look-ahead: while warps 1.. apply the trailing
+// update of panel p, warp 0 updates the next 16x16 diagonal block first and factors/inverts it, so the
+// sequential diagonal work of panel p+1 overlaps the tensor-core work of panel p. Returns false as soon as GEPP
+// would interchange rows (T is then partially overwritten and must be re-staged). PIVOT = true: GEPP, no
+// look-ahead.
+template <bool PIVOT, int NWARPS>
+__device__ __forceinline__ bool phase_a(double* T, const Geo& geo, double* Uinv_all, double* Linv, int* piv,
+                                        int* flag, int* spec, int tid, int warp, int lane, uint64_t* mbarB = nullptr,
+                                        uint32_t ph = 0, long long* trace = nullptr, int64_t tit = 0) {
+  const int ne = geo.ne, R = geo.R8, C8 = geo.C8, ldT = geo.ldT;
+  const int npan = (ne + NB - 1) / NB;
+  if (!PIVOT && warp == 0) {      // prologue: diagonal block of panel 0 (needs only the A rows)
+    if (diag_factor(T, ldT, 0, min(NB, ne), Linv, Uinv_all, Linv + NB * LDI, lane) && lane == 0) *spec = 1;
+  }
+  if (mbarB) mbar_wait(mbarB, ph);   // B_e / r_e columns (streamed in during the prologue)
+  for (int p = 0; p < npan; ++p) {
+    const int jb = p * NB, nb = min(NB, ne - jb);
+    double* Uinv = Uinv_all + p * NB * LDI;
+    if (PIVOT && warp == 0) {
+      panel_factor_pivot(T, ldT, jb, nb, ne, piv, flag, lane);
+      __syncwarp();
+      diag_inverses(T, ldT, jb, nb, Linv, Uinv, lane);
     }
-    if (tid == 0) *flag = 0;
     __syncthreads();
-
-    // ---- a2 (+ forward part of a3): blocked LU with partial pivoting ---------------------------------------
-    for (int p = 0; p < npan; ++p) {
-      const int jb = p * kNB, nb = min(kNB, ne - jb);
-      if (warp == 0) panel_factor(T, ldT, P, ldP, jb, nb, ne, piv, rcp, flag, lane);
-      __syncthreads();
-      // row interchanges outside the panel + U12 = L11^-1 A12 (thread per column)
-      for (int j = tid; j < C8; j += THREADS) {
+    HDG_STAMP(trace, tit, 16 + 3 * p);
+    if (!PIVOT && *spec) return false;
+    if (PIVOT) {   // interchanges of this panel applied to all other columns (thread per column)
+      for (int j = tid; j < C8; j += NWARPS * 32) {
         if (j >= jb && j < jb + nb) continue;
         for (int c = 0; c < nb; ++c) {
           const int pr = piv[jb + c];
@@ -184,47 +391,172 @@ __global__ void __launch_bounds__(THREADS) condense_kernel(const CondenseArgs a)
             T[pr * ldT + j] = t;
           }
         }
-        if (j >= jb + nb) {
-          double t[kNB];
-#pragma unroll
-          for (int c = 0; c < kNB; ++c) t[c] = c < nb ? T[(jb + c) * ldT + j] : 0.0;
-#pragma unroll
-          for (int c = 0; c < kNB; ++c)
-#pragma unroll
-            for (int c2 = c + 1; c2 < kNB; ++c2)
-              if (c2 < nb) t[c2] -= T[(jb + c2) * ldT + jb + c] * t[c];
-#pragma unroll
-          for (int c = 1; c < kNB; ++c)
-            if (c < nb) T[(jb + c) * ldT + j] = t[c];
-        }
       }
       __syncthreads();
-      if (jb + nb < ne) {
-        mma_update<NWARPS>(T, T + jb, T + jb * ldT, ldT, jb + nb, R8, jb + nb, C8, nb, warp, lane);
-        __syncthreads();
+    }
+    // U12 = L11^-1 A12 (column tiles right of the panel) and, on the fast path, L21 = A21 U11^-1 (row tiles
+    // below the panel), distributed over the warps
+    const int cj0 = (jb + NB) >> 3, ncj = (C8 >> 3) - cj0;
+    const int ri0 = (jb + NB) >> 3, nri = PIVOT ? 0 : (R >> 3) - ri0;
+    bool viol = false;
+    for (int job = warp; job < ncj + nri; job += NWARPS) {
+      if (job < ncj) inv_times_tile(T, ldT, jb, Linv, (cj0 + job) * 8, lane);
+      else viol |= tile_times_uinv(T, ldT, jb, Uinv, (ri0 + job - ncj) * 8, lane);
+    }
+    if (!PIVOT && __any_sync(0xffffffffu, viol) && lane == 0) *spec = 1;
+    __syncthreads();
+    HDG_STAMP(trace, tit, 17 + 3 * p);
+    if (!PIVOT && *spec) return false;
+    if (jb + NB < R) {
+      const int nk = (nb + 3) & ~3;
+      if (PIVOT) {
+        mma_update(T, T + jb, T + jb * ldT, ldT, jb + NB, R, jb + NB, C8, nk, warp, NWARPS, lane);
+      } else if (warp == 0) {
+        // block 0 of the trailing region = the next diagonal block: update it, then factor and invert it
+        mma_update(T, T + jb, T + jb * ldT, ldT, jb + NB, R, jb + NB, C8, nk, 0, 1, lane, 1);
+        __syncwarp();
+        const int jn = jb + NB, nn = min(NB, ne - jn);
+        if (diag_factor(T, ldT, jn, nn, Linv, Uinv_all + (p + 1) * NB * LDI, Linv + NB * LDI, lane) && lane == 0)
+          *spec = 1;
+      } else {
+        mma_update(T, T + jb, T + jb * ldT, ldT, jb + NB, R, jb + NB, C8, nk, warp, NWARPS - 1, lane);
       }
+      HDG_STAMP(trace, tit, 18 + 3 * p);
+      if (PIVOT) __syncthreads();
+    }
+  }
+  return true;
+}
+
+template <int NWARPS>
+__device__ __forceinline__ void stage(double* T, const Geo& geo, const double* A, const double* Bm, const double* re,
+                                      int warp, int lane) {
+  const int ne = geo.ne, nf = geo.nf, R = geo.R8, CB = geo.CB, C8 = geo.C8, ldT = geo.ldT;
+  for (int i = warp; i < R; i += NWARPS) {
+    double* Ti = T + i * ldT;
+    if (i < ne) {
+      const double2* Ai = reinterpret_cast<const double2*>(A + (int64_t)i * ne);
+      for (int j = lane; j < ne / 2; j += 32) reinterpret_cast<double2*>(Ti)[j] = __ldg(Ai + j);
+      for (int j = ne + lane; j < CB; j += 32) Ti[j] = 0.0;
+      const double2* Bi = reinterpret_cast<const double2*>(Bm + (int64_t)i * nf);
+      for (int j = lane; j < nf / 2; j += 32) reinterpret_cast<double2*>(Ti + CB)[j] = __ldg(Bi + j);
+      if (lane == 0) Ti[CB + nf] = __ldg(re + i);
+      for (int j = CB + nf + 1 + lane; j < C8; j += 32) Ti[j] = 0.0;
+    } else {
+      for (int j = lane; j < C8; j += 32) Ti[j] = 0.0;
+    }
+  }
+}
+
+// one warp issues `rows` bulk copies of `bytes` each (row i: src + i*lds -> dst + i*ldd), all counted on bar
+__device__ __forceinline__ void issue_rows(double* dst, int ldd, const double* src, int64_t lds, int rows, int cols,
+                                           uint64_t* bar, int lane) {
+  if (lane == 0) mbar_expect_tx(bar, (uint32_t)rows * (uint32_t)cols * 8u);
+  __syncwarp();
+  for (int i = lane; i < rows; i += 32) bulk_g2s(dst + i * ldd, src + (int64_t)i * lds, (uint32_t)cols * 8u, bar);
+}
+
+constexpr int kChunkCT = 8;   // column tiles of [S | g] per pass of phase B
+constexpr int kBatchK = 16;   // k4-steps of C_e fragments loaded ahead in phase B
+
+template <int THREADS, int MINB, bool T_SMEM>
+__global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseArgs a) {
+  constexpr int NWARPS = THREADS / 32;
+  extern __shared__ __align__(16) double smem[];
+  const Geo geo(a.ne, a.nf);
+  const int ne = geo.ne, nf = geo.nf, CB = geo.CB, C8 = geo.C8, ldT = geo.ldT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npan = (ne + NB - 1) / NB;
+  double* T = T_SMEM ? smem : a.scratch + (int64_t)blockIdx.x * geo.t_doubles();
+  double* Uinv_all = T_SMEM ? smem + geo.t_doubles() : smem;
+  double* Linv = Uinv_all + npan * NB * LDI;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(Linv + NB * LDI + 48);   // [0]: A rows, [1]: B rows
+  int* piv = reinterpret_cast<int*>(mbar + 2);
+  int* flag = piv + geo.R8;
+  int* spec = flag + 1;
+
+  auto elem_of = [&](int64_t it) -> int64_t { return a.elems ? a.elems[it] : it; };
+  // start streaming [A | B] of an element into T; r_e with ordinary loads (one column)
+  auto issue_A = [&](int64_t l) { issue_rows(T, ldT, a.A + a.offA[l], ne, ne, ne, &mbar[0], lane); };
+  auto issue_B = [&](int64_t l) { issue_rows(T + CB, ldT, a.B + a.offB[l], nf, ne, nf, &mbar[1], lane); };
+  auto load_re = [&](int64_t l) {
+    for (int i = tid; i < ne; i += THREADS) T[i * ldT + CB + nf] = __ldg(a.re + a.offRe[l] + i);
+  };
+
+  if (T_SMEM) {
+    // zero T once: the padding rows/columns stay zero through every element (see phase comments)
+    for (int i = tid; i < geo.t_doubles(); i += THREADS) T[i] = 0.0;
+    if (tid == 0) {
+      mbar_init(&mbar[0]);
+      mbar_init(&mbar[1]);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (blockIdx.x < a.count) {
+      const int64_t l0 = elem_of(blockIdx.x);
+      if (warp == 0) {
+        issue_A(l0);
+        issue_B(l0);
+      }
+      load_re(l0);
+    }
+  }
+  uint32_t ph = 0;
+
+  for (int64_t it = blockIdx.x; it < a.count; it += gridDim.x, ph ^= 1u) {
+    const int64_t l = elem_of(it);
+    const double* A = a.A + a.offA[l];
+    const double* Bm = a.B + a.offB[l];
+    const double* re = a.re + a.offRe[l];
+    const int64_t next = it + gridDim.x;
+
+    // ---- a1 stage + a2 (+ forward part of a3) --------------------------------------------------------------
+    if (!T_SMEM) stage<NWARPS>(T, geo, A, Bm, re, warp, lane);
+    if (tid == 0) { *flag = 0; *spec = 0; }
+    const int64_t tit = (it - blockIdx.x) / gridDim.x;
+    HDG_STAMP(a.trace, tit, 0);
+    if (T_SMEM) mbar_wait(&mbar[0], ph);
+    HDG_STAMP(a.trace, tit, 1);
+    __syncthreads();
+    HDG_STAMP(a.trace, tit, 2);
+    bool pivoted = false;
+    if (!phase_a<false, NWARPS>(T, geo, Uinv_all, Linv, piv, flag, spec, tid, warp, lane,
+                                T_SMEM ? &mbar[1] : nullptr, ph, a.trace, tit)) {
+      pivoted = true;
+      __syncthreads();
+      stage<NWARPS>(T, geo, A, Bm, re, warp, lane);
+      if (tid == 0) { *flag = 0; *spec = 0; }
+      __syncthreads();
+      phase_a<true, NWARPS>(T, geo, Uinv_all, Linv, piv, flag, spec, tid, warp, lane);
     }
     const int fail = *flag;
+    HDG_STAMP(a.trace, tit, 3);
 
     // ---- a5 factors: L\U column-major + row permutation -----------------------------------------------------
     {
-      unsigned char* fb = a.factors + a.offF[l];
-      double* LU = reinterpret_cast<double*>(fb);
+      double* LU = reinterpret_cast<double*>(a.factors + a.offF[l]);
       // lanes cover a 4 (rows) x 8 (cols) micro-tile: conflict-free smem reads, full 32-byte sector writes
-      const int ib = (ne + 3) / 4, kb = (ne + 7) / 8;
-      for (int t = warp; t < ib * kb; t += NWARPS) {
-        const int i = (t % ib) * 4 + (lane & 3), k = (t / ib) * 8 + (lane >> 2);
-        if (k < ne) LU[(int64_t)k * ne + i] = T[i * ldT + k];
-      }
-      if (tid == 0) {
-        int32_t* perm = reinterpret_cast<int32_t*>(LU + (int64_t)ne * ne);
-        for (int i = 0; i < ne; ++i) perm[i] = i;
-        for (int k = 0; k < ne; ++k) {
-          const int pr = piv[k];
-          if (pr != k) { const int32_t t = perm[k]; perm[k] = perm[pr]; perm[pr] = t; }
+      const int ib = ne / 4, kb = (ne + 7) / 8;
+      for (int kt = 0; kt < kb; ++kt) {
+        const int k = kt * 8 + (lane >> 2);
+        for (int t = warp; t < ib; t += NWARPS) {
+          const int i = t * 4 + (lane & 3);
+          if (k < ne) LU[(int64_t)k * ne + i] = T[i * ldT + k];
         }
-        a.info[l] = fail;
       }
+      // row permutation of P A: follow where original row i ends up through the interchanges (parallel in i)
+      int32_t* perm = reinterpret_cast<int32_t*>(LU + (int64_t)ne * ne);
+      for (int i = tid; i < ne; i += THREADS) {
+        int pos = i;
+        if (pivoted)
+          for (int k = 0; k < ne; ++k) {
+            const int pr = piv[k];
+            if (pos == k) pos = pr;
+            else if (pos == pr) pos = k;
+          }
+        perm[pos] = i;
+      }
+      if (tid == 0) a.info[l] = fail;
     }
 
     double* S = a.S + a.offS[l];
@@ -233,51 +565,49 @@ __global__ void __launch_bounds__(THREADS) condense_kernel(const CondenseArgs a)
       for (int i = tid; i < nf * nf; i += THREADS) S[i] = __longlong_as_double(0x7ff8000000000000LL);
       for (int i = tid; i < nf; i += THREADS) g[i] = __longlong_as_double(0x7ff8000000000000LL);
       __syncthreads();
-      continue;
-    }
-
-    // ---- a3 backward part: X = U^-1 W on columns [CB, C8), panels bottom-up -----------------------------------
-    for (int p = npan - 1; p >= 0; --p) {
-      const int jb = p * kNB, nb = min(kNB, ne - jb);
-      for (int j = CB + tid; j < C8; j += THREADS) {
-        double t[kNB];
-#pragma unroll
-        for (int c = 0; c < kNB; ++c) t[c] = c < nb ? T[(jb + c) * ldT + j] : 0.0;
-#pragma unroll
-        for (int c = kNB - 1; c >= 0; --c) {
-          if (c < nb) {
-            t[c] *= rcp[jb + c];
-#pragma unroll
-            for (int c2 = 0; c2 < c; ++c2) t[c2] -= T[(jb + c2) * ldT + jb + c] * t[c];
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < kNB; ++c)
-          if (c < nb) T[(jb + c) * ldT + j] = t[c];
-      }
+      if (T_SMEM)   // NaNs may have reached the padding: restore the zeros
+        for (int i = tid; i < geo.t_doubles(); i += THREADS) T[i] = 0.0;
       __syncthreads();
-      if (jb > 0) {
-        mma_update<NWARPS>(T, T + jb, T + jb * ldT, ldT, 0, jb, CB, C8, nb, warp, lane);
+    } else {
+      HDG_STAMP(a.trace, tit, 4);
+      // ---- a3 backward part: X = U^-1 W on columns [CB, C8), panels bottom-up ---------------------------------
+      for (int p = npan - 1; p >= 0; --p) {
+        const int jb = p * NB, nb = min(NB, ne - jb);
+        const double* Uinv = Uinv_all + p * NB * LDI;
+        for (int job = warp; job < ((C8 - CB) >> 3); job += NWARPS) inv_times_tile(T, ldT, jb, Uinv, CB + job * 8, lane);
         __syncthreads();
+        if (jb > 0) {
+          mma_update(T, T + jb, T + jb * ldT, ldT, 0, jb, CB, C8, (nb + 3) & ~3, warp, NWARPS, lane);
+          __syncthreads();
+        }
       }
+    }
+    HDG_STAMP(a.trace, tit, 5);
+    // the A columns of T are free from here on: start streaming the next element's A_e
+    if (T_SMEM && warp == 0 && next < a.count) {
+      fence_proxy_async();
+      issue_A(elem_of(next));
     }
 
     // ---- a4 Schur complement: [S | g] = [D | r_f] - C X, one warp per 8-row tile, DMMA over k = n_e ----------
-    {
+    if (!fail) {
       const double* Cm = a.C + a.offC[l];
       const double* D = a.D + a.offD[l];
       const double* rf = a.rf + a.offRf[l];
       const int RTs = (nf + 7) >> 3, CTs = (C8 - CB) >> 3;
+      const int nchunk = (CTs + kChunkCT - 1) / kChunkCT;
       const int gid = lane >> 2, tig = lane & 3;
-      for (int tr = warp; tr < RTs; tr += NWARPS) {
+      for (int wi = warp; wi < RTs * nchunk; wi += NWARPS) {
+        const int tr = wi / nchunk, ch = wi - tr * nchunk;
         const int row = tr * 8 + gid;
         const bool rv = row < nf;
-        double acc[kMaxCT][2];
+        const int j0 = ch * kChunkCT;
+        double acc[kChunkCT][2];
 #pragma unroll
-        for (int j = 0; j < kMaxCT; ++j) {
-          const int c = 8 * j + 2 * tig;
+        for (int j = 0; j < kChunkCT; ++j) {
+          const int c = 8 * (j0 + j) + 2 * tig;
           double v0 = 0.0, v1 = 0.0;
-          if (j < CTs && rv) {
+          if (j0 + j < CTs && rv) {
             if (c < nf) { const double2 d = *reinterpret_cast<const double2*>(D + (int64_t)row * nf + c); v0 = d.x; v1 = d.y; }
             else if (c == nf) v0 = rf[row];
           }
@@ -285,19 +615,29 @@ __global__ void __launch_bounds__(THREADS) condense_kernel(const CondenseArgs a)
           acc[j][1] = v1;
         }
         const double* Crow = Cm + (int64_t)(rv ? row : 0) * ne;
-#pragma unroll 4
-        for (int k = 0; k < ne; k += 4) {
-          const double av = rv ? -__ldg(Crow + k + tig) : 0.0;
-          const double* Tk = T + (k + tig) * ldT + CB + gid;
+        for (int k0 = 0; k0 < ne; k0 += 4 * kBatchK) {
+          double cv[kBatchK];
 #pragma unroll
-          for (int j = 0; j < kMaxCT; ++j)
-            if (j < CTs) dmma(acc[j], av, Tk[8 * j]);
+          for (int q = 0; q < kBatchK; ++q) {
+            const int k = k0 + 4 * q;
+            cv[q] = (rv && k < ne) ? -__ldg(Crow + k + tig) : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < kBatchK; ++q) {
+            const int k = k0 + 4 * q;
+            if (k < ne) {
+              const double* Tk = T + (k + tig) * ldT + CB + 8 * j0 + gid;
+#pragma unroll
+              for (int j = 0; j < kChunkCT; ++j)
+                if (j0 + j < CTs) dmma(acc[j], cv[q], Tk[8 * j]);
+            }
+          }
         }
         if (rv) {
 #pragma unroll
-          for (int j = 0; j < kMaxCT; ++j) {
-            const int c = 8 * j + 2 * tig;
-            if (j < CTs) {
+          for (int j = 0; j < kChunkCT; ++j) {
+            const int c = 8 * (j0 + j) + 2 * tig;
+            if (j0 + j < CTs) {
               if (c < nf) *reinterpret_cast<double2*>(S + (int64_t)row * nf + c) = make_double2(acc[j][0], acc[j][1]);
               else if (c == nf) g[row] = acc[j][0];
             }
@@ -305,25 +645,36 @@ __global__ void __launch_bounds__(THREADS) condense_kernel(const CondenseArgs a)
         }
       }
     }
+    HDG_STAMP(a.trace, tit, 6);
     __syncthreads();
+    HDG_STAMP(a.trace, tit, 7);
+    // X has been consumed: stream the next element's B_e and r_e into the right-hand columns
+    if (T_SMEM && next < a.count) {
+      const int64_t ln = elem_of(next);
+      if (warp == 0) {
+        fence_proxy_async();
+        issue_B(ln);
+      }
+      load_re(ln);
+    }
   }
 }
 
-template <int THREADS, bool T_SMEM>
+template <int THREADS, int MINB, bool T_SMEM>
 cudaError_t launch_t(const CondenseArgs& a, int sms, cudaStream_t s) {
   const Geo geo(a.ne, a.nf);
   const int64_t smem = geo.smem_bytes(T_SMEM);
-  cudaError_t e = cudaFuncSetAttribute(condense_kernel<THREADS, T_SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kern = condense_kernel<THREADS, MINB, T_SMEM>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, condense_kernel<THREADS, T_SMEM>, THREADS, (size_t)smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, (size_t)smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = (int64_t)sms * per_sm;
   if (!T_SMEM) grid = sms;   // one scratch slab per resident CTA
   if (grid > a.count) grid = a.count;
-  condense_kernel<THREADS, T_SMEM><<<(unsigned)grid, THREADS, (size_t)smem, s>>>(a);
+  kern<<<(unsigned)grid, THREADS, (size_t)smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -332,10 +683,11 @@ cudaError_t launch_t(const CondenseArgs& a, int sms, cudaStream_t s) {
 cudaError_t launch_condense(const CondenseArgs& a, bool t_in_smem, int sms, cudaStream_t s, int64_t* launches) {
   if (a.count <= 0) return cudaSuccess;
   ++*launches;
-  if (!t_in_smem) return launch_t<256, false>(a, sms, s);
-  if (a.ne <= 16) return launch_t<64, true>(a, sms, s);
-  if (a.ne <= 32) return launch_t<128, true>(a, sms, s);
-  return launch_t<256, true>(a, sms, s);
+  if (!t_in_smem) return launch_t<256, 1, false>(a, sms, s);
+  if (a.ne <= 16) return launch_t<64, 6, true>(a, sms, s);
+  if (a.ne <= 32) return launch_t<128, 3, true>(a, sms, s);
+  if (a.ne <= 64) return launch_t<128, 2, true>(a, sms, s);
+  return launch_t<256, 1, true>(a, sms, s);
 }
 
 }  // namespace hdg

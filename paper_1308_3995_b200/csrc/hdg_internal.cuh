@@ -18,23 +18,23 @@ constexpr int kMaxCT = (kMaxNf + 1 + 7) / 8;   // column tiles of [S | g] in pha
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-// Geometry of the per-element working matrix T = [A | pad | B | r_e | pad] (rows padded to R8 with zeros).
-// Columns: A at [0, ne), B at [CB, CB+nf), r_e at CB+nf, zero padding up to C8; row stride ldT = 4 mod 16
-// doubles so that DMMA A-, B- and C-fragment accesses are shared-memory bank-conflict free.
+// Geometry of the per-element working matrix T = [A | 0 | B | r_e | 0] (rows padded with zeros to R8, a
+// multiple of 16). Columns: A at [0, ne), B at CB = round_up(ne, 16), r_e at CB+nf, zero padding up to C8;
+// row stride ldT = 4 mod 16 doubles so that DMMA A-, B- and C-fragment accesses are bank-conflict free.
 struct Geo {
-  int ne, nf, R8, CB, NC, C8, ldT, ldP;
+  int ne, nf, R8, CB, NC, C8, ldT;
   __host__ __device__ Geo(int ne_, int nf_) : ne(ne_), nf(nf_) {
-    R8 = round_up(ne, 8);
+    R8 = round_up(ne, 16);
     CB = R8;
     NC = CB + nf + 1;
     C8 = round_up(NC, 8);
     ldT = round_up(C8 - 4, 16) + 4;
-    ldP = R8 + 1;
   }
   __host__ __device__ int64_t t_doubles() const { return (int64_t)R8 * ldT; }
-  // shared memory of the condensation kernel: [T (if in smem)] [P: panel, col-major] [rcp] [piv] [flag]
+  // shared memory of the condensation kernel: [T (if in smem)] [U11^-1 per panel] [L11^-1] [48 doubles broadcast buffer] [2 mbarriers] [piv] [flag, spec]
   __host__ __device__ int64_t smem_bytes(bool t_in_smem) const {
-    return 8 * ((t_in_smem ? t_doubles() : 0) + (int64_t)kNB * ldP + R8) + 4 * (int64_t)R8 + 16;
+    const int npan = (ne + kNB - 1) / kNB;
+    return 8 * ((t_in_smem ? t_doubles() : 0) + (int64_t)(npan + 1) * kNB * 20 + 48 + 2) + 4 * (int64_t)R8 + 16;
   }
 };
 
@@ -51,6 +51,7 @@ struct CondenseArgs {
   int ne, nf;
   int64_t count;
   double* scratch;        // global workspace for T when it does not fit in shared memory
+  long long* trace;       // instrumentation: clock64 stamps of CTA 0 (NULL = off)
 };
 
 struct BacksubArgs {
@@ -118,6 +119,7 @@ struct hdg_ctx_s {
   std::string last_error;
   hdg::Plan plan;
   int64_t launches = 0;
+  long long* trace = nullptr;
 };
 
 // kernel launchers (defined in the .cu files); return cudaError_t of the launch
