@@ -48,29 +48,31 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// dst[r][c] -= sum_{k < nk} As[r][k] * Bs[k][c] over rows [r_lo, r_hi) and columns [c_lo, c_hi) (multiples of 8;
-// nk multiple of 4). dst, As, Bs share the row stride ld. Work unit: a 2x2 block of 8x8 tiles per warp.
-// Blocks are numbered row-major over the 16x16 grid; this warp takes blocks first, first + stride, ...
+// dst[r][c] -= sum_{k < nk} As[r][k] * Bs[k][c] over rows [r_lo, r_hi) (multiples of 16) and columns
+// [c_lo, c_hi) (multiples of 8); nk multiple of 4. dst, As, Bs share the row stride ld. Work unit: a 16 x 32
+// block (2 x 4 tiles of 8x8) per warp, so each k-step loads 2 A- and 4 B-fragments for 8 DMMAs and every
+// accumulator tile is read and written once per call. Blocks are numbered row-major; this warp takes blocks
+// first, first + stride, ... (at most max_blocks of them).
 __device__ __forceinline__ void mma_update(double* dst, const double* As, const double* Bs, int ld, int r_lo, int r_hi,
                                            int c_lo, int c_hi, int nk, int first, int stride, int lane,
                                            int max_blocks = 1 << 30) {
-  const int RT = (r_hi - r_lo) >> 3, CT = (c_hi - c_lo) >> 3;
-  if (RT <= 0 || CT <= 0) return;
-  const int BR = (RT + 1) >> 1, BC = (CT + 1) >> 1;
+  const int BR = (r_hi - r_lo) >> 4, CT = (c_hi - c_lo) >> 3;
+  if (BR <= 0 || CT <= 0) return;
+  const int BC = (CT + 3) >> 2;
   const int nblk = min(BR * BC, max_blocks);
   const int gid = lane >> 2, tig = lane & 3;
   for (int blk = first; blk < nblk; blk += stride) {
     const int br = blk / BC, bc = blk - br * BC;
-    const int r0 = r_lo + br * 16, c0 = c_lo + bc * 16;
-    const bool two_r = (br * 2 + 1) < RT, two_c = (bc * 2 + 1) < CT;
-    double acc[2][2][2];
+    const int r0 = r_lo + br * 16, c0 = c_lo + bc * 32;
+    const int nct = min(4, CT - 4 * bc);
+    double acc[2][4][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < 4; ++j) {
         acc[i][j][0] = 0.0;
         acc[i][j][1] = 0.0;
-        if ((i == 0 || two_r) && (j == 0 || two_c)) {
+        if (j < nct) {
           const double2 v = *reinterpret_cast<const double2*>(dst + (r0 + 8 * i + gid) * ld + c0 + 8 * j + 2 * tig);
           acc[i][j][0] = v.x;
           acc[i][j][1] = v.y;
@@ -78,23 +80,29 @@ __device__ __forceinline__ void mma_update(double* dst, const double* As, const 
       }
     for (int k = 0; k < nk; k += 4) {
       const double a0 = -As[(r0 + gid) * ld + k + tig];
-      const double a1 = two_r ? -As[(r0 + 8 + gid) * ld + k + tig] : 0.0;
-      const double b0 = Bs[(k + tig) * ld + c0 + gid];
-      const double b1 = two_c ? Bs[(k + tig) * ld + c0 + 8 + gid] : 0.0;
-      dmma(acc[0][0], a0, b0);
-      dmma(acc[0][1], a0, b1);
-      dmma(acc[1][0], a1, b0);
-      dmma(acc[1][1], a1, b1);
+      const double a1 = -As[(r0 + 8 + gid) * ld + k + tig];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j < nct) {
+          const double b = Bs[(k + tig) * ld + c0 + 8 * j + gid];
+          dmma(acc[0][j], a0, b);
+          dmma(acc[1][j], a1, b);
+        }
+      }
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
-        if ((i == 0 || two_r) && (j == 0 || two_c))
+      for (int j = 0; j < 4; ++j)
+        if (j < nct)
           *reinterpret_cast<double2*>(dst + (r0 + 8 * i + gid) * ld + c0 + 8 * j + 2 * tig) =
               make_double2(acc[i][j][0], acc[i][j][1]);
   }
 }
+
+// Phase A' for one column tile (8 columns at c0) of W, entirely inside one warp (no CTA barriers): panels
+// bottom-up, X_p = U_pp^-1 W_p, then W_<p -= U_<p,p X_p for this tile only.
+__device__ __forceinline__ void backsolve_tile(double* T, int ldT, int ne, const double* Uinv_all, int c0, int lane);
 
 // 1/x with one MUFU.RCP64H and two Newton steps (no slow path; pivots here are finite and non-zero, a zero or
 // non-finite pivot is caught by the GEPP speculation check and redone on the pivoting path).
@@ -107,91 +115,84 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, e, r);
 }
 
-// Fast path: factor the nb x nb diagonal block at (jb, jb) in natural row order and invert both factors, one
-// warp, laid out by COLUMNS: lane j < 16 holds column j of D, lane 16 + j column j of the identity. Step c: lane
-// c forms the multipliers of column c and publishes them in `buf` (shared memory broadcast); every trailing D
-// column and every identity column applies the row operations, so the forward pass maps [D | I] to
-// [L\U | L^-1]. U^-1 then comes from a backward substitution of the identity columns against U (read from T).
-// FULL: nb == 16 (compile-time trip counts, no bounds checks). Linv/Uinv: row-major 16x16, stride LDI, zero
-// padded beyond nb. Returns true if GEPP would have interchanged rows (|a_ik| > |a_kk|, i > k) or a pivot is 0.
-template <bool FULL>
-__device__ __forceinline__ bool diag_factor_t(double* T, int ldT, int jb, int nb_in, double* Linv, double* Uinv,
-                                              double* buf, int lane) {
-  const int nb = FULL ? NB : nb_in;
-  const int j = lane & 15;
-  const bool dl = lane < 16;
-  const bool valid = j < nb;
+// Fast path: factor the 16x16 diagonal block at (jb, jb) in natural row order and invert both factors, one
+// warp. A partial block (nb < 16, last panel) is padded with identity rows/columns, so L11^-1 and U11^-1 carry
+// ones on the padded diagonal (harmless: the padded rows/columns of T are zero).
+//   forward:  lane r < 16 holds row r in registers; step c broadcasts the pivot row (shuffles), every lower row
+//             forms its multiplier and updates itself -> L\U (written back to T, rows < nb only);
+//   inverses: lane c < 16 solves L x = e_c (column c of L11^-1); lane 16 + c solves the index-reversed lower
+//             system J U J z = e_(15-c) (column c of U11^-1 = J z); one instruction stream, lane-dependent
+//             addresses, right-looking substitution with the factors read from T (broadcast loads).
+// Linv/Uinv: row-major 16x16, stride LDI. Returns true if GEPP would have interchanged rows (|a_ik| > |a_kk|,
+// i > k) or a pivot is zero.
+__device__ __forceinline__ bool diag_factor(double* T, int ldT, int jb, int nb, double* Linv, double* Uinv, int lane) {
+  double d[NB];
+  double* rcs = Linv + NB * LDI;   // 16 pivot reciprocals (shared memory: keeps them out of the register file)
+  const bool real = lane < nb;
   double* Dg = T + jb * ldT + jb;
-  double x[NB];
+  const double2* src = reinterpret_cast<const double2*>(Dg + (real ? lane : 0) * ldT);
 #pragma unroll
-  for (int i = 0; i < NB; ++i) {
-    const bool in = FULL || (valid && i < nb);
-    x[i] = dl ? (in ? Dg[i * ldT + j] : 0.0) : ((i == j) ? 1.0 : 0.0);
+  for (int j = 0; j < NB; j += 2) {
+    double2 v = make_double2(j == lane ? 1.0 : 0.0, j + 1 == lane ? 1.0 : 0.0);   // identity padding
+    if (real) v = src[j / 2];
+    d[j] = v.x;
+    d[j + 1] = v.y;
   }
   bool viol = false;
-  // reciprocal of the pivot of step 0 (lane 0); later pivots' reciprocals are formed right after their final
-  // update in the previous step, overlapping the rest of that step's row operations
-  double rnext = fast_rcp(x[0]);
 #pragma unroll
   for (int c = 0; c < NB; ++c) {
-    if (!FULL && c >= nb) break;
-    double* bc = buf + (c & 1) * 16;             // double-buffered broadcast slot
-    if (lane == c) {
-      const double pv = x[c];
-      viol |= !(fabs(pv) > 0.0);
+    double prow[NB];
 #pragma unroll
-      for (int i = c + 1; i < NB; ++i) {
-        viol |= fabs(x[i]) > fabs(pv);
-        const double m = x[i] * rnext;
-        x[i] = m;
-        bc[i] = m;
-      }
-    }
-    __syncwarp();
-    const double xc = x[c];
-    if (!dl || j > c) {
-      if (c + 1 < NB) {
-        x[c + 1] = fma(-bc[c + 1], xc, x[c + 1]);
-        rnext = fast_rcp(x[c + 1]);              // used by lane c+1 in step c+1
-      }
+    for (int j = c; j < NB; ++j) prow[j] = __shfl_sync(0xffffffffu, d[j], c);
+    const double pv = prow[c];
+    viol |= pv == 0.0;
+    const double rp = fast_rcp(pv);
+    if (lane == 0) rcs[c] = rp;
+    if (lane > c && lane < NB) {
+      viol |= fabs(d[c]) > fabs(pv);
+      const double l = d[c] * rp;
+      d[c] = l;
 #pragma unroll
-      for (int i = c + 2; i < NB; ++i) x[i] = fma(-bc[i], xc, x[i]);
+      for (int j = c + 1; j < NB; ++j) d[j] = fma(-l, prow[j], d[j]);
     }
   }
-  if (dl) {
-    if (FULL || valid) {
+  // the identity-padded factors go to a scratch copy of the block (Linv's storage is reused after), T gets
+  // only the real rows
+  double* F = Uinv;   // 16 x LDI scratch: overwritten by U^-1 below, after all lanes have read it
+  if (lane < NB) {
+    double2* dst = reinterpret_cast<double2*>(F + lane * LDI);
 #pragma unroll
-      for (int i = 0; i < NB; ++i)
-        if (FULL || i < nb) Dg[i * ldT + j] = x[i];
-      buf[32 + j] = fast_rcp(x[j]);          // 1 / u_jj
+    for (int j = 0; j < NB; j += 2) dst[j / 2] = make_double2(d[j], d[j + 1]);
+    if (real) {
+      double2* dt = reinterpret_cast<double2*>(Dg + lane * ldT);
+#pragma unroll
+      for (int j = 0; j < NB; j += 2) dt[j / 2] = make_double2(d[j], d[j + 1]);
     }
-  } else {
-#pragma unroll
-    for (int i = 0; i < NB; ++i) Linv[i * LDI + j] = (FULL || (valid && i < nb)) ? x[i] : 0.0;
   }
   __syncwarp();
-  // U^-1: column j solves U y = e_j (identity lanes), U read back from T (broadcast loads)
-  if (!dl) {
+  const bool up = lane >= 16;
+  const int c = lane & 15;
+  const double* mp = up ? F + (NB - 1) * LDI + (NB - 1) : F;     // m_ik = mp[sg * (i * LDI + k)]
+  const int sg = up ? -1 : 1;
+  double x[NB];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) x[i] = (i == j) ? 1.0 : 0.0;
+  for (int i = 0; i < NB; ++i) x[i] = (i == (up ? NB - 1 - c : c)) ? 1.0 : 0.0;
 #pragma unroll
-    for (int c = NB - 1; c >= 0; --c) {
-      if (FULL || c < nb) {
-        x[c] *= buf[32 + c];
+  for (int k = 0; k < NB; ++k) {
+    double m[NB];
 #pragma unroll
-        for (int i = 0; i < c; ++i) x[i] = fma(-Dg[i * ldT + c], x[c], x[i]);
-      }
-    }
+    for (int i = k + 1; i < NB; ++i) m[i] = mp[sg * (i * LDI + k)];
+    const double rk = rcs[NB - 1 - k];
+    asm volatile("" ::: "memory");   // keep the column's loads here (bounded register pressure)
+    if (up) x[k] *= rk;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) Uinv[i * LDI + j] = (FULL || (valid && i < nb)) ? x[i] : 0.0;
+    for (int i = k + 1; i < NB; ++i) x[i] = fma(-m[i], x[k], x[i]);
   }
+  __syncwarp();   // all reads of the scratch factors done before U^-1 overwrites it
+  double* op = up ? Uinv + (NB - 1) * LDI + c : Linv + c;         // row i of this lane's system -> op[sg * i * LDI]
+#pragma unroll
+  for (int i = 0; i < NB; ++i) op[sg * i * LDI] = x[i];
   return __any_sync(0xffffffffu, viol);
-}
-
-__device__ __forceinline__ bool diag_factor(double* T, int ldT, int jb, int nb, double* Linv, double* Uinv,
-                                            double* buf, int lane) {
-  return nb == NB ? diag_factor_t<true>(T, ldT, jb, nb, Linv, Uinv, buf, lane)
-                  : diag_factor_t<false>(T, ldT, jb, nb, Linv, Uinv, buf, lane);
 }
 
 // Pivoting path: inverses of the factored diagonal block already in T (L11\U11 at (jb, jb)), same registers
@@ -264,6 +265,41 @@ __device__ __forceinline__ void inv_times_tile(double* T, int ldT, int jb, const
 #pragma unroll
   for (int i = 0; i < 2; ++i)
     *reinterpret_cast<double2*>(T + (jb + 8 * i + gid) * ldT + c0 + 2 * tig) = make_double2(acc[i][0], acc[i][1]);
+}
+
+__device__ __forceinline__ void backsolve_tile(double* T, int ldT, int ne, const double* Uinv_all, int c0, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  const int npan = (ne + NB - 1) / NB;
+  for (int p = npan - 1; p >= 0; --p) {
+    const int jb = p * NB;
+    inv_times_tile(T, ldT, jb, Uinv_all + p * NB * LDI, c0, lane);
+    __syncwarp();
+    if (jb == 0) break;
+    const int nk4 = (min(NB, ne - jb) + 3) >> 2;
+    double xb[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) xb[kk] = kk < nk4 ? T[(jb + 4 * kk + tig) * ldT + c0 + gid] : 0.0;
+    for (int r0 = 0; r0 < jb; r0 += 16) {        // two row tiles per iteration: independent DMMA chains
+      double acc[2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double2 v = *reinterpret_cast<const double2*>(T + (r0 + 8 * i + gid) * ldT + c0 + 2 * tig);
+        acc[i][0] = v.x;
+        acc[i][1] = v.y;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (kk < nk4) {
+          dmma(acc[0], -T[(r0 + gid) * ldT + jb + 4 * kk + tig], xb[kk]);
+          dmma(acc[1], -T[(r0 + 8 + gid) * ldT + jb + 4 * kk + tig], xb[kk]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        *reinterpret_cast<double2*>(T + (r0 + 8 * i + gid) * ldT + c0 + 2 * tig) = make_double2(acc[i][0], acc[i][1]);
+    }
+    __syncwarp();
+  }
 }
 
 // T[r0..r0+8, jb..jb+16) <- T[r0..r0+8, jb..jb+16) * Uinv, in place (L21 = A21 U11^-1); one warp, one row tile.
@@ -353,6 +389,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// bulk prefetch of a global range into L2 (TMA engine; no shared memory involved)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // Phase A. PIVOT = false: speculative natural-order pass with look-ahead: while warps 1.. apply the trailing
 // update of panel p, warp 0 updates the next 16x16 diagonal block first and factors/inverts it, so the
@@ -366,7 +406,7 @@ __device__ __forceinline__ bool phase_a(double* T, const Geo& geo, double* Uinv_
   const int ne = geo.ne, R = geo.R8, C8 = geo.C8, ldT = geo.ldT;
   const int npan = (ne + NB - 1) / NB;
   if (!PIVOT && warp == 0) {      // prologue: diagonal block of panel 0 (needs only the A rows)
-    if (diag_factor(T, ldT, 0, min(NB, ne), Linv, Uinv_all, Linv + NB * LDI, lane) && lane == 0) *spec = 1;
+    if (diag_factor(T, ldT, 0, min(NB, ne), Linv, Uinv_all, lane) && lane == 0) *spec = 1;
   }
   if (mbarB) mbar_wait(mbarB, ph);   // B_e / r_e columns (streamed in during the prologue)
   for (int p = 0; p < npan; ++p) {
@@ -412,14 +452,18 @@ __device__ __forceinline__ bool phase_a(double* T, const Geo& geo, double* Uinv_
       if (PIVOT) {
         mma_update(T, T + jb, T + jb * ldT, ldT, jb + NB, R, jb + NB, C8, nk, warp, NWARPS, lane);
       } else if (warp == 0) {
-        // block 0 of the trailing region = the next diagonal block: update it, then factor and invert it
-        mma_update(T, T + jb, T + jb * ldT, ldT, jb + NB, R, jb + NB, C8, nk, 0, 1, lane, 1);
+        // the next diagonal block first (16 x 16), then factor and invert it (look-ahead)
+        mma_update(T, T + jb, T + jb * ldT, ldT, jb + NB, jb + 2 * NB, jb + NB, jb + 2 * NB, nk, 0, 1, lane);
         __syncwarp();
         const int jn = jb + NB, nn = min(NB, ne - jn);
-        if (diag_factor(T, ldT, jn, nn, Linv, Uinv_all + (p + 1) * NB * LDI, Linv + NB * LDI, lane) && lane == 0)
-          *spec = 1;
+        if (diag_factor(T, ldT, jn, nn, Linv, Uinv_all + (p + 1) * NB * LDI, lane) && lane == 0) *spec = 1;
       } else {
-        mma_update(T, T + jb, T + jb * ldT, ldT, jb + NB, R, jb + NB, C8, nk, warp, NWARPS - 1, lane);
+        // the rest of the trailing region: rows of the next panel right of its diagonal block, then all rows below
+        const int w = warp - 1, nw = NWARPS - 1;
+        const int nb_a = (C8 - jb - 2 * NB + 31) >> 5;               // 16x32 blocks in region (a)
+        mma_update(T, T + jb, T + jb * ldT, ldT, jb + NB, jb + 2 * NB, jb + 2 * NB, C8, nk, w, nw, lane);
+        const int first_b = ((w - nb_a) % nw + nw) % nw;             // continue the round-robin in region (b)
+        mma_update(T, T + jb, T + jb * ldT, ldT, jb + 2 * NB, R, jb + NB, C8, nk, first_b, nw, lane);
       }
       HDG_STAMP(trace, tit, 18 + 3 * p);
       if (PIVOT) __syncthreads();
@@ -458,6 +502,77 @@ __device__ __forceinline__ void issue_rows(double* dst, int ldd, const double* s
 
 constexpr int kChunkCT = 8;   // column tiles of [S | g] per pass of phase B
 constexpr int kBatchK = 16;   // k4-steps of C_e fragments loaded ahead in phase B
+
+// Phase B work: NI work items (8-row tile of [S | g] x chunk of kChunkCT column tiles) per warp at a time; all
+// their D / r_f / C loads are issued before the first DMMA and the NI independent accumulator sets interleave.
+template <int NI, int NWARPS>
+__device__ __forceinline__ void schur_items(const double* T, int ldT, int ne, int nf, int CB, int CTs, int nchunk,
+                                            const double* Cm, const double* D, const double* rf, double* S, double* g,
+                                            int warp, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nItems = ((nf + 7) >> 3) * nchunk;
+  for (int w0 = warp; w0 < nItems; w0 += NI * NWARPS) {
+    int row[NI], j0[NI];
+    bool rv[NI];
+    const double* Crow[NI];
+    double acc[NI][kChunkCT][2];
+    double cv[NI][kBatchK];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int wi = (w0 + i * NWARPS < nItems) ? w0 + i * NWARPS : w0;
+      const int tr = wi / nchunk, ch = wi - tr * nchunk;
+      row[i] = tr * 8 + gid;
+      rv[i] = (w0 + i * NWARPS < nItems) && row[i] < nf;
+      j0[i] = ch * kChunkCT;
+      const int rc = rv[i] ? row[i] : 0;
+      Crow[i] = Cm + (int64_t)rc * ne;
+      const double rfv = __ldg(rf + rc);
+#pragma unroll
+      for (int j = 0; j < kChunkCT; ++j) {
+        const int c = 8 * (j0[i] + j) + 2 * tig;
+        const double2 dv = __ldg(reinterpret_cast<const double2*>(D + (int64_t)rc * nf + min(c, nf - 2)));
+        const bool on = rv[i] && (j0[i] + j < CTs);
+        acc[i][j][0] = on ? (c < nf ? dv.x : (c == nf ? rfv : 0.0)) : 0.0;
+        acc[i][j][1] = (on && c < nf) ? dv.y : 0.0;
+      }
+    }
+    for (int k0 = 0; k0 < ne; k0 += 4 * kBatchK) {
+      // every load of the batch is issued before any use (no arithmetic on the loaded values here, so they
+      // stay in flight together); out-of-range k is clamped, padded rows are zeroed at use
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+#pragma unroll
+        for (int q = 0; q < kBatchK; ++q) cv[i][q] = __ldg(Crow[i] + min(k0 + 4 * q, ne - 4) + tig);
+#pragma unroll
+      for (int q = 0; q < kBatchK; ++q) {
+        const int k = k0 + 4 * q;
+        if (k < ne) {
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            const double av = rv[i] ? -cv[i][q] : 0.0;
+            const double* Tk = T + (k + tig) * ldT + CB + 8 * j0[i] + gid;
+#pragma unroll
+            for (int j = 0; j < kChunkCT; ++j)
+              if (j0[i] + j < CTs) dmma(acc[i][j], av, Tk[8 * j]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      if (rv[i]) {
+#pragma unroll
+        for (int j = 0; j < kChunkCT; ++j) {
+          const int c = 8 * (j0[i] + j) + 2 * tig;
+          if (j0[i] + j < CTs) {
+            if (c < nf) *reinterpret_cast<double2*>(S + (int64_t)row[i] * nf + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+            else if (c == nf) g[row[i]] = acc[i][j][0];
+          }
+        }
+      }
+    }
+  }
+}
 
 template <int THREADS, int MINB, bool T_SMEM>
 __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseArgs a) {
@@ -514,6 +629,11 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
     if (!T_SMEM) stage<NWARPS>(T, geo, A, Bm, re, warp, lane);
     if (tid == 0) { *flag = 0; *spec = 0; }
     const int64_t tit = (it - blockIdx.x) / gridDim.x;
+    // phase B reads C_e, D_e, r_f long after they are needed by nothing else: pull them into L2 now
+    if (tid == 32) {
+      prefetch_l2(a.C + a.offC[l], (uint32_t)(nf * ne * 8));
+      prefetch_l2(a.D + a.offD[l], (uint32_t)(nf * nf * 8));
+    }
     HDG_STAMP(a.trace, tit, 0);
     if (T_SMEM) mbar_wait(&mbar[0], ph);
     HDG_STAMP(a.trace, tit, 1);
@@ -571,16 +691,8 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
     } else {
       HDG_STAMP(a.trace, tit, 4);
       // ---- a3 backward part: X = U^-1 W on columns [CB, C8), panels bottom-up ---------------------------------
-      for (int p = npan - 1; p >= 0; --p) {
-        const int jb = p * NB, nb = min(NB, ne - jb);
-        const double* Uinv = Uinv_all + p * NB * LDI;
-        for (int job = warp; job < ((C8 - CB) >> 3); job += NWARPS) inv_times_tile(T, ldT, jb, Uinv, CB + job * 8, lane);
-        __syncthreads();
-        if (jb > 0) {
-          mma_update(T, T + jb, T + jb * ldT, ldT, 0, jb, CB, C8, (nb + 3) & ~3, warp, NWARPS, lane);
-          __syncthreads();
-        }
-      }
+      for (int ct = warp; ct < ((C8 - CB) >> 3); ct += NWARPS) backsolve_tile(T, ldT, ne, Uinv_all, CB + ct * 8, lane);
+      __syncthreads();
     }
     HDG_STAMP(a.trace, tit, 5);
     // the A columns of T are free from here on: start streaming the next element's A_e
@@ -596,54 +708,10 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
       const double* rf = a.rf + a.offRf[l];
       const int RTs = (nf + 7) >> 3, CTs = (C8 - CB) >> 3;
       const int nchunk = (CTs + kChunkCT - 1) / kChunkCT;
-      const int gid = lane >> 2, tig = lane & 3;
-      for (int wi = warp; wi < RTs * nchunk; wi += NWARPS) {
-        const int tr = wi / nchunk, ch = wi - tr * nchunk;
-        const int row = tr * 8 + gid;
-        const bool rv = row < nf;
-        const int j0 = ch * kChunkCT;
-        double acc[kChunkCT][2];
-#pragma unroll
-        for (int j = 0; j < kChunkCT; ++j) {
-          const int c = 8 * (j0 + j) + 2 * tig;
-          double v0 = 0.0, v1 = 0.0;
-          if (j0 + j < CTs && rv) {
-            if (c < nf) { const double2 d = *reinterpret_cast<const double2*>(D + (int64_t)row * nf + c); v0 = d.x; v1 = d.y; }
-            else if (c == nf) v0 = rf[row];
-          }
-          acc[j][0] = v0;
-          acc[j][1] = v1;
-        }
-        const double* Crow = Cm + (int64_t)(rv ? row : 0) * ne;
-        for (int k0 = 0; k0 < ne; k0 += 4 * kBatchK) {
-          double cv[kBatchK];
-#pragma unroll
-          for (int q = 0; q < kBatchK; ++q) {
-            const int k = k0 + 4 * q;
-            cv[q] = (rv && k < ne) ? -__ldg(Crow + k + tig) : 0.0;
-          }
-#pragma unroll
-          for (int q = 0; q < kBatchK; ++q) {
-            const int k = k0 + 4 * q;
-            if (k < ne) {
-              const double* Tk = T + (k + tig) * ldT + CB + 8 * j0 + gid;
-#pragma unroll
-              for (int j = 0; j < kChunkCT; ++j)
-                if (j0 + j < CTs) dmma(acc[j], cv[q], Tk[8 * j]);
-            }
-          }
-        }
-        if (rv) {
-#pragma unroll
-          for (int j = 0; j < kChunkCT; ++j) {
-            const int c = 8 * (j0 + j) + 2 * tig;
-            if (j0 + j < CTs) {
-              if (c < nf) *reinterpret_cast<double2*>(S + (int64_t)row * nf + c) = make_double2(acc[j][0], acc[j][1]);
-              else if (c == nf) g[row] = acc[j][0];
-            }
-          }
-        }
-      }
+      if (RTs * nchunk > NWARPS)
+        schur_items<2, NWARPS>(T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, S, g, warp, lane);
+      else
+        schur_items<1, NWARPS>(T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, S, g, warp, lane);
     }
     HDG_STAMP(a.trace, tit, 6);
     __syncthreads();
