@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -57,6 +58,17 @@ void free_plan(Plan& p) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// HDG_CONDENSE_KERNEL=panel|sweep forces one condensation kernel for every bucket it supports (A/B comparisons,
+// tests of both paths)
+bool force_panel() {
+  const char* v = getenv("HDG_CONDENSE_KERNEL");
+  return v && strcmp(v, "panel") == 0;
+}
+bool force_sweep() {
+  const char* v = getenv("HDG_CONDENSE_KERNEL");
+  return v && strcmp(v, "sweep") == 0;
+}
 
 }  // namespace
 
@@ -196,7 +208,14 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     B.count = (int64_t)b.second.size();
     const Geo geo(B.ne, B.nf);
     B.t_in_smem = geo.smem_bytes(true) <= (int64_t)ctx->smem_optin;
-    if (!B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
+    // the sweep kernel (one element per SM, chain warp + MMA workers) wins from n_e ~ 96 up (C4: 46 vs 57 ms);
+    // below, the panel kernel with several CTAs per SM is faster (C3: 34 vs 47 ms) — measured on the box
+    B.sweep = sweep_supported(B.ne, B.nf, ctx->smem_optin) && !force_panel() && (B.ne >= 96 || force_sweep());
+    if (!B.sweep && !B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
+    if (B.sweep) {   // exact-path slab per resident CTA (at most 2 per SM)
+      const SweepGeo sg(B.ne, B.nf);
+      scratch = std::max(scratch, ((int64_t)sg.RA * sg.ldT + (int64_t)sg.NF8 * sg.ldC) * 2 * ctx->sms);
+    }
     HDG_CUDA(ctx, upload(&B.d_elems, b.second.data(), b.second.size()));
     p.buckets.push_back(B);
   }
@@ -329,7 +348,9 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
     a.ne = b.ne; a.nf = b.nf; a.count = b.count;
     a.scratch = p.d_scratch;
     a.trace = ctx->trace;
-    HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
+    a.debug = getenv("HDG_DEBUG_MODE") ? atoi(getenv("HDG_DEBUG_MODE")) : 0;
+    if (b.sweep) HDG_CUDA(ctx, launch_condense_sweep(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
+    else HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
   }
   return HDG_OK;
 }

@@ -2,12 +2,12 @@
 //
 //     u_e = A_e^-1 (r_e - B_e lambda_e)          (Eq. ls; "reconstructed inside the elements",
 //                                                 PAPER.md:357-359; "reconstruct_local")
-// using the factorization saved by hdg_condense: L\U column-major + the row permutation.
+// using the factorization saved by hdg_condense: L\U row-major + the row permutation.
 //
 // HBM-bound streaming kernel, one warp per element, nothing staged in shared memory except lambda_e and the
 // permutation buffer: lane i owns rows i, i+32, ... in registers; the triangular solves are column-oriented
-// (column k of L or U is contiguous in the column-major factor, so each step is one coalesced warp load plus a
-// shuffle broadcast of x_k). Many warps per SM hide the n_e-step dependency chain.
+// (step k: one shuffle broadcast of x_k, every lane reads element (i, k) of its rows — consecutive k hit the
+// same L1 lines of the row-major factor). Many warps per SM hide the n_e-step dependency chain.
 #include "hdg_internal.cuh"
 
 namespace hdg {
@@ -77,22 +77,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) backsub_kernel(const Back
       const int i = lane + 32 * s;
       rd[s] = i < ne ? 1.0 / __ldg(LU + (int64_t)i * ne + i) : 0.0;
     }
-    // forward: L y = P t (unit lower), column k of L = LU[k*ne + i], i > k
+    // forward: L y = P t (unit lower), column k of L = LU[i*ne + k], i > k
 #pragma unroll
     for (int s = 0; s < MAXR; ++s) {
       for (int lk = 0; lk < 32; ++lk) {
         const int k = 32 * s + lk;
         if (k >= ne) break;
         const double xk = __shfl_sync(0xffffffffu, t[s], lk);
-        const double* Lk = LU + (int64_t)k * ne;
+        const double* Lk = LU + k;
 #pragma unroll
         for (int s2 = s; s2 < MAXR; ++s2) {
           const int i = lane + 32 * s2;
-          if (i > k && i < ne) t[s2] = fma(-__ldg(Lk + i), xk, t[s2]);
+          if (i > k && i < ne) t[s2] = fma(-__ldg(Lk + (int64_t)i * ne), xk, t[s2]);
         }
       }
     }
-    // backward: U x = y, column k of U = LU[k*ne + i], i < k
+    // backward: U x = y, column k of U = LU[i*ne + k], i < k
 #pragma unroll
     for (int s = MAXR - 1; s >= 0; --s) {
       for (int lk = 31; lk >= 0; --lk) {
@@ -100,11 +100,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) backsub_kernel(const Back
         if (k >= ne) continue;
         if (lane == lk) t[s] *= rd[s];
         const double xk = __shfl_sync(0xffffffffu, t[s], lk);
-        const double* Uk = LU + (int64_t)k * ne;
+        const double* Uk = LU + k;
 #pragma unroll
         for (int s2 = 0; s2 <= s; ++s2) {
           const int i = lane + 32 * s2;
-          if (i < k) t[s2] = fma(-__ldg(Uk + i), xk, t[s2]);
+          if (i < k) t[s2] = fma(-__ldg(Uk + (int64_t)i * ne), xk, t[s2]);
         }
       }
     }

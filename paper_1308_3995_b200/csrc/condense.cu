@@ -20,7 +20,7 @@
 //              Pivoting path: one warp factors the whole panel column by column with the GEPP pivot search
 //              (maximal |a_ik|, lowest index on ties), interchanges are applied to the
 //              other columns, then U12 and the trailing update as above.
-//   factors  : L\U written column-major + the row permutation (for hdg_backsubstitute).
+//   factors  : L\U written row-major + the row permutation (for hdg_backsubstitute).
 //   phase A' : X = U^-1 [L^-1 P B | L^-1 P r_e] = A_e^-1 [B_e | r_e] by blocked backward substitution, panels
 //              bottom-up: X_p = U_pp^-1 W_p and W_<p -= U_<p,p X_p, both DMMA.
 //   phase B  : [S_e | g_e] = [D_e | r_f] - C_e X, DMMA GEMM n_f x (n_f+1) x n_e per element; C_e, D_e read from
@@ -652,18 +652,10 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
     const int fail = *flag;
     HDG_STAMP(a.trace, tit, 3);
 
-    // ---- a5 factors: L\U column-major + row permutation -----------------------------------------------------
+    // ---- a5 factors: L\U row-major + row permutation ---------------------------------------------------------
     {
       double* LU = reinterpret_cast<double*>(a.factors + a.offF[l]);
-      // lanes cover a 4 (rows) x 8 (cols) micro-tile: conflict-free smem reads, full 32-byte sector writes
-      const int ib = ne / 4, kb = (ne + 7) / 8;
-      for (int kt = 0; kt < kb; ++kt) {
-        const int k = kt * 8 + (lane >> 2);
-        for (int t = warp; t < ib; t += NWARPS) {
-          const int i = t * 4 + (lane & 3);
-          if (k < ne) LU[(int64_t)k * ne + i] = T[i * ldT + k];
-        }
-      }
+      for (int idx = tid; idx < ne * ne; idx += THREADS) LU[idx] = T[(idx / ne) * ldT + idx % ne];
       // row permutation of P A: follow where original row i ends up through the interchanges (parallel in i)
       int32_t* perm = reinterpret_cast<int32_t*>(LU + (int64_t)ne * ne);
       for (int i = tid; i < ne; i += THREADS) {

@@ -38,7 +38,36 @@ struct Geo {
   }
 };
 
-// Opaque per-element factor record: [LU of P A_e, column-major, ne*ne doubles][perm: ne int32][pad to 16 B].
+// Smallest row stride >= cols (doubles) that is 4 or 12 mod 16: every DMMA A/B-fragment load (8-byte, lanes
+// (gid, tig) -> row gid / k tig) of a 16-lane phase then hits 32 distinct banks.
+__host__ __device__ constexpr int pad_ld(int cols) {
+  return (cols % 16 <= 4) ? cols - cols % 16 + 4 : (cols % 16 <= 12 ? cols - cols % 16 + 12 : cols - cols % 16 + 20);
+}
+
+// Geometry of the sweep condensation kernel (condense_sweep.cu): T = [A | 0 | B | r_e | 0] with RA = round8(n_e)
+// rows (zero padding rows), B at column CB = round8(n_e), NCAB = CB + round8(n_f + 1) columns used; the C_e rows
+// in a second region Cr of NF8 = round8(n_f) rows x CB columns. [S | g] is CTs = round8(n_f + 1) / 8 column tiles.
+struct SweepGeo {
+  int ne, nf, RA, CB, NCAB, ldT, NF8, ldC, CTs, npan, ntiles;
+  __host__ __device__ SweepGeo(int ne_, int nf_) : ne(ne_), nf(nf_) {
+    RA = round_up(ne, 8);
+    CB = RA;
+    NCAB = CB + round_up(nf + 1, 8);
+    ldT = pad_ld(NCAB);
+    NF8 = round_up(nf, 8);
+    ldC = pad_ld(CB);
+    CTs = round_up(nf + 1, 8) / 8;
+    npan = (ne + kNB - 1) / kNB;
+    ntiles = (NF8 / 8) * CTs;
+  }
+  // [T][Cr][L11^-1 x2][U11^-1 x2][2 broadcast slots of 40] doubles, 4 mbarriers, piv[RA], fail flag (+pad)
+  __host__ __device__ int64_t smem_bytes() const {
+    return 8 * ((int64_t)RA * ldT + (int64_t)NF8 * ldC + 4 * kNB * 20 + 80) + 8 * 4 + 4 * (int64_t)RA + 16;
+  }
+};
+
+// Opaque per-element factor record: [LU of P A_e, row-major, ne*ne doubles][perm: ne int32][pad to 16 B];
+// perm[i] = the row of A_e that is row i of P A_e.
 __host__ __device__ inline int64_t factor_bytes(int ne) { return ((int64_t)ne * ne * 8 + (int64_t)ne * 4 + 15) / 16 * 16; }
 
 struct CondenseArgs {
@@ -52,6 +81,7 @@ struct CondenseArgs {
   int64_t count;
   double* scratch;        // global workspace for T when it does not fit in shared memory
   long long* trace;       // instrumentation: clock64 stamps of CTA 0 (NULL = off)
+  int debug;              // profiling experiments only (HDG_DEBUG_MODE): 1 = workers skip their MMA work
 };
 
 struct BacksubArgs {
@@ -72,7 +102,8 @@ struct Bucket {
   int ne, nf;
   int64_t count;
   int32_t* d_elems;   // device list of local element ids
-  bool t_in_smem;
+  bool t_in_smem;     // panel kernel: working matrix in shared memory (else global scratch)
+  bool sweep;         // condensed by the sweep kernel (condense_sweep.cu)
 };
 
 // Skeleton assembly data (owned rows).
@@ -125,6 +156,8 @@ struct hdg_ctx_s {
 // kernel launchers (defined in the .cu files); return cudaError_t of the launch
 namespace hdg {
 cudaError_t launch_condense(const CondenseArgs& a, bool t_in_smem, int sms, cudaStream_t s, int64_t* launches);
+bool sweep_supported(int ne, int nf, size_t smem_optin);
+cudaError_t launch_condense_sweep(const CondenseArgs& a, int sms, size_t smem_optin, cudaStream_t s, int64_t* launches);
 cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s);
 cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, double* K, double* E, double* send,

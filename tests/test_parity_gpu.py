@@ -238,3 +238,42 @@ def test_device_generator_bit_identical(cuda):
     raw = gen.device_philox_raw([[0, 0, 0, 0], [0xFFFFFFFF] * 4], [[0, 0], [0xFFFFFFFF] * 2])
     assert [hex(x) for x in raw[0]] == ["0x6627e8d5", "0xe169c58d", "0xbc57ac4c", "0x9b00dbd8"]
     assert [hex(x) for x in raw[1]] == ["0x408f276d", "0x41c83b0e", "0xa20bc7c6", "0x6d5451fd"]
+
+
+@pytest.fixture(params=["sweep", "panel"])
+def kernel(request, monkeypatch):
+    """Force one condensation kernel for every bucket it supports (read by hdg_plan)."""
+    monkeypatch.setenv("HDG_CONDENSE_KERNEL", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("name,nr,nt", [("C1", 3, 5), ("C2", 4, 9), ("C3", 5, 9), ("C4", 4, 9)])
+def test_both_condense_kernels(cuda, kernel, name, nr, nt):
+    """Each condensation kernel (sweep: one element per SM with register-resident [S|g]; panel: several CTAs
+    per SM) is held to the same bar on every uniform config's block sizes, whichever one the plan would pick."""
+    check_all(gen.config(name, nr=nr, nt=nt))
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_both_kernels_pivot_forcing(cuda, kernel, name):
+    """P9 on both kernels: permuted rows force the exact (pivoting) path; a zero-ish leading entry too."""
+    w = gen.config(name, nr=2, nt=4)
+    blk = gen.host_blocks(w)
+    rng = np.random.default_rng(7)
+    for e in range(w.E):
+        ne, nf = int(w.elem_ne[e]), int(w.elem_nf[e])
+        A = blk["A"][blk["off_A"][e]:blk["off_A"][e + 1]].reshape(ne, ne)
+        B = blk["B"][blk["off_B"][e]:blk["off_B"][e + 1]].reshape(ne, nf)
+        re = blk["re"][blk["off_re"][e]:blk["off_re"][e + 1]]
+        if e % 2 == 0:       # every other element pivots: fast and exact paths interleave in one CTA
+            P = rng.permutation(ne)
+            A[...] = A[P]
+            B[...] = B[P]
+            re[...] = re[P]
+    check_all(w, blk=blk)
+
+
+def test_sweep_hp_buckets(cuda, monkeypatch):
+    """configs[4] with the sweep kernel forced: its supported (n_e, n_f) buckets next to panel-kernel buckets."""
+    monkeypatch.setenv("HDG_CONDENSE_KERNEL", "sweep")
+    check_all(gen.config("C5", nr=5, nt=10))
