@@ -170,6 +170,80 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def setup_workload(config: str, rank: int = 0, world: int = 1, local: int = 0, slab=None):
+    """The benchmark's launch configuration (shared with the full-size parity tests): this rank's element slab of
+    the BASELINE config, inputs generated directly in HBM (bit-identical to gen.host_blocks), plan built once,
+    outputs allocated. slab = (r, P): emulate rank r of a P-way partition on this single GPU (used for C5, whose
+    full mesh needs ~490 GB: rank 0 of 8 is one B200's share at N = 8; its shared-face rows get only the local
+    contributions, the exchange step is not run)."""
+    import torch
+    import gen
+    import paper_1308_3995_b200 as hdg
+    dev = torch.device("cuda", local)
+    w = gen.config(config)
+    if slab is not None:
+        r_emul, p_emul = slab
+        reb = slab_bounds(w.E, p_emul)
+        eb, n = int(reb[r_emul]), int(reb[r_emul + 1] - reb[r_emul])
+        ctx = hdg.Context(local, r_emul, p_emul)
+        info = ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne, eb, n, reb)
+    else:
+        reb = slab_bounds(w.E, world)
+        eb, n = int(reb[rank]), int(reb[rank + 1] - reb[rank])
+        ctx = hdg.Context(local, rank, world)
+        info = ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne, eb, n, reb if world > 1 else None)
+    stream = torch.cuda.Stream(dev)
+    inp = {}
+    with torch.cuda.stream(stream):
+        dne = torch.from_numpy(w.elem_ne[eb:eb + n].copy()).to(dev)
+        dnf = torch.from_numpy(w.elem_nf[eb:eb + n].copy()).to(dev)
+        for k in ("A", "B", "C", "D", "re", "rf"):
+            o = w.off[k][eb:eb + n + 1] - w.off[k][eb]
+            inp[k] = torch.empty(max(int(o[-1]), 2), dtype=torch.float64, device=dev)
+            if w.uniform:
+                gen.device_blocks(w, k, inp[k], e0=eb, n=n, stream=stream.cuda_stream)
+            else:
+                gen.device_blocks(w, k, inp[k], e0=eb, n=n, off=torch.from_numpy(o).to(dev), stream=stream.cuda_stream,
+                                  dev_ne=dne, dev_nf=dnf)
+        lam = torch.empty(w.n_trace, dtype=torch.float64, device=dev)
+        gen.device_lambda(w, lam, torch.from_numpy(w.face_ndof).to(dev), torch.from_numpy(w.face_off).to(dev))
+    out = dict(w=w, ctx=ctx, info=info, stream=stream, inp=inp, lam=lam, eb=eb, n=n, reb=reb, world=world,
+               exchange=(world > 1 and slab is None))
+    for k in ("S", "g", "u", "factors", "info", "K", "E"):
+        out[{"factors": "F", "info": "infot"}.get(k, k)] = ctx.alloc(k)
+    out["send"] = ctx.alloc("send") if info.send_doubles > 0 else None
+    out["recv"] = ctx.alloc("recv") if info.recv_doubles > 0 else None
+    return out
+
+
+def run_step(wl, ev=None):
+    """One step of the hot path on the workload; returns the libhdg launches issued."""
+    import paper_1308_3995_b200 as hdg
+    ctx, stream, inp = wl["ctx"], wl["stream"], wl["inp"]
+    n = 0
+    if ev:
+        ev[0].record(stream)
+    ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], wl["S"], wl["g"], wl["F"], wl["infot"],
+                 stream=stream)
+    n += ctx.launch_count()
+    if ev:
+        ev[1].record(stream)
+    ctx.assemble_skeleton(wl["S"], wl["g"], wl["K"], wl["E"], send=wl["send"], stream=stream)
+    n += ctx.launch_count()
+    if wl["exchange"]:
+        stream.synchronize()
+        hdg.exchange(ctx, wl["send"], wl["recv"])
+        ctx.skeleton_accumulate(wl["recv"], wl["K"], wl["E"], stream=stream)
+        n += ctx.launch_count()
+    if ev:
+        ev[2].record(stream)
+    ctx.backsubstitute(wl["F"], inp["B"], inp["re"], wl["lam"], wl["u"], stream=stream)
+    n += ctx.launch_count()
+    if ev:
+        ev[3].record(stream)
+    return n
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -181,7 +255,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--slab", default=None,
+                    help="r/P: time rank r's slab of a P-way partition on this one GPU (default for C5: 0/8)")
     args = ap.parse_args()
+    if args.slab is None and args.config == "C5" and int(os.environ.get("WORLD_SIZE", "1")) < 4:
+        args.slab = "0/8"      # C5 (~490 GB) does not fit one B200: one rank's share of the 8-GPU partition
+    if args.slab is not None:
+        r_, p_ = (int(x) for x in args.slab.split("/"))
+        args.slab = (r_, p_)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -200,57 +281,19 @@ def main():
     dev = torch.device("cuda", local)
     dmma_peak, dfma_peak = (fp64_peak_in_run() if rank == 0 else (None, None))
 
-    w = gen.config(args.config)
-    reb = slab_bounds(w.E, world)
-    eb, n = int(reb[rank]), int(reb[rank + 1] - reb[rank])
-    ctx = hdg.Context(local, rank, world)
-    info = ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne, eb, n, reb if world > 1 else None)
-    stream = torch.cuda.Stream(dev)
-
-    # inputs generated in HBM for this rank's slab (same bytes as gen.host_blocks)
-    inp = {}
-    with torch.cuda.stream(stream):
-        dne = torch.from_numpy(w.elem_ne[eb:eb + n].copy()).to(dev)
-        dnf = torch.from_numpy(w.elem_nf[eb:eb + n].copy()).to(dev)
-        for k in ("A", "B", "C", "D", "re", "rf"):
-            o = w.off[k][eb:eb + n + 1] - w.off[k][eb]
-            inp[k] = torch.empty(max(int(o[-1]), 2), dtype=torch.float64, device=dev)
-            if w.uniform:
-                gen.device_blocks(w, k, inp[k], e0=eb, n=n, stream=stream.cuda_stream)
-            else:
-                gen.device_blocks(w, k, inp[k], e0=eb, n=n, off=torch.from_numpy(o).to(dev), stream=stream.cuda_stream,
-                                  dev_ne=dne, dev_nf=dnf)
-        lam = torch.empty(w.n_trace, dtype=torch.float64, device=dev)
-        gen.device_lambda(w, lam, torch.from_numpy(w.face_ndof).to(dev), torch.from_numpy(w.face_off).to(dev))
-    S, g, u = ctx.alloc("S"), ctx.alloc("g"), ctx.alloc("u")
-    F, infot = ctx.alloc("factors"), ctx.alloc("info")
-    K, E = ctx.alloc("K"), ctx.alloc("E")
-    send = ctx.alloc("send") if info.send_doubles > 0 else None
-    recv = ctx.alloc("recv") if info.recv_doubles > 0 else None
+    wl = setup_workload(args.config, rank, world, local, slab=args.slab)
+    w, ctx, info, stream, inp, lam = wl["w"], wl["ctx"], wl["info"], wl["stream"], wl["inp"], wl["lam"]
+    S, g, u, F, infot, K, E, send, recv = (wl[k] for k in ("S", "g", "u", "F", "infot", "K", "E", "send", "recv"))
+    eb, n, reb = wl["eb"], wl["n"], wl["reb"]
+    elems = n if args.slab is not None else w.E     # elements one step processes (all ranks together)
+    workload = args.config if args.slab is None else (f"{args.config} slab {args.slab[0]}/{args.slab[1]} "
+                                                      f"(elements [{eb}, {eb + n}) of {w.E})")
     torch.cuda.synchronize()
 
     launches = [0]
 
     def step(ev=None):
-        if ev:
-            ev[0].record(stream)
-        ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], S, g, F, infot, stream=stream)
-        launches[0] += ctx.launch_count()
-        if ev:
-            ev[1].record(stream)
-        ctx.assemble_skeleton(S, g, K, E, send=send, stream=stream)
-        launches[0] += ctx.launch_count()
-        if world > 1:
-            stream.synchronize()
-            hdg.exchange(ctx, send, recv)
-            ctx.skeleton_accumulate(recv, K, E, stream=stream)
-            launches[0] += ctx.launch_count()
-        if ev:
-            ev[2].record(stream)
-        ctx.backsubstitute(F, inp["B"], inp["re"], lam, u, stream=stream)
-        launches[0] += ctx.launch_count()
-        if ev:
-            ev[3].record(stream)
+        launches[0] += run_step(wl, ev)
 
     for _ in range(args.warmup):
         step()
@@ -325,7 +368,7 @@ def main():
         te = torch.tensor([a.elapsed_time(b) / ke2e], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": w.E / (te.item() / 1e3), "unit": "elements/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": elems / (te.item() / 1e3), "unit": "elements/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": ke2e,
                "note": "host (pinned) inputs A,B,C,D,r_e,r_f,lambda copied in and K,E,u copied out every step"}
 
@@ -364,17 +407,17 @@ def main():
         except Exception:
             pass
         line = {
-            "metric": METRIC, "value": w.E / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": world,
+            "metric": METRIC, "value": elems / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Philox blocks with BASELINE.json distributions, generated in HBM)",
-            "config": {"workload": args.config, "elements": w.E, "n_e": int(w.elem_ne.max()),
-                       "n_f": int(w.elem_nf.max()), "faces": w.F, "trace_dofs": w.n_trace,
+            "config": {"workload": workload, "elements": elems, "n_e": int(w.elem_ne[eb:eb + n].max()),
+                       "n_f": int(w.elem_nf[eb:eb + n].max()), "faces": w.F, "trace_dofs": w.n_trace,
                        "parallelism": f"element slabs x{world}" + (" + NCCL shared-face exchange" if world > 1 else ""),
                        "l2": "inputs (%.1f GB/rank) exceed the 126 MB L2; no flush needed" % (
                            sum(v.numel() for v in inp.values()) * 8 / 1e9),
                        "step": "condense + assemble_skeleton + backsubstitute"},
-            "condense_per_s": w.E / (cond_ms * 1e-3), "backsub_per_s": w.E / (bs_ms * 1e-3),
+            "condense_per_s": elems / (cond_ms * 1e-3), "backsub_per_s": elems / (bs_ms * 1e-3),
             "condense_ms": cond_ms, "assemble_ms": asm_ms, "backsub_ms": bs_ms,
             "backsub_hbm_gbs": work["backsub_bytes"] / (bs_ms * 1e-3) / 1e9,
             "roofline": roof,
