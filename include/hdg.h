@@ -133,6 +133,20 @@ hdg_status hdg_assemble_skeleton(hdg_ctx ctx, const double* S, const double* g, 
 hdg_status hdg_exchange_counts(hdg_ctx ctx, int64_t* send_counts, int64_t* send_displs, int64_t* recv_counts,
                                int64_t* recv_displs);
 
+/* a7 exchange layout, host only (no device, no context: usable for planning and by CPU tests of the multi-rank
+ * path). All pointers [host]. mesh: as for hdg_plan, rank_elem_begin required. Per peer rank (arrays of nranks):
+ * doubles sent/received and their offsets in the packed buffers (same values hdg_exchange_counts reports after
+ * hdg_plan). Items, [n][3] int64 each, NULL to query the counts only:
+ *   send_items: (global face f, LOCAL element l, offset o): send[o .. o + n_fp) = g_l[slot f], then the
+ *               n_fp x n_f(l) strip S_l[slot f rows, all columns] row-major — face f's row is owned by the rank
+ *               of its left element, which is remote;
+ *   recv_items: (owned face f, GLOBAL remote element e, offset o), same packing, added after the owner's own
+ *               contribution by hdg_skeleton_accumulate (left, then right).
+ * Items are grouped by peer rank, then face id. Returns HDG_ERR_ARG on inconsistent arguments. */
+hdg_status hdg_exchange_layout(const hdg_mesh* mesh, int rank, int nranks, int64_t* send_counts, int64_t* send_displs,
+                               int64_t* recv_counts, int64_t* recv_displs, int64_t* n_send_items, int64_t* send_items,
+                               int64_t* n_recv_items, int64_t* recv_items);
+
 /* a7 finish: add the contributions received from other ranks (recv, device, plan.recv_doubles) into the owned
  * rows, after this rank's own (left) contributions: the result is bitwise identical to one rank. */
 hdg_status hdg_skeleton_accumulate(hdg_ctx ctx, const double* recv, double* K, double* E, hdg_stream stream);

@@ -86,6 +86,8 @@ def lib():
         L.hdg_debug_set_trace.argtypes = [P, P]
         L.hdg_max_elem_ndof.restype = I32
         L.hdg_max_face_ndof.restype = I32
+        L.hdg_exchange_layout.restype = I32
+        L.hdg_exchange_layout.argtypes = [ctypes.POINTER(_Mesh), I32, I32] + [P] * 8
         _lib = L
     return _lib
 
@@ -93,7 +95,7 @@ def lib():
 EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status_string", "hdg_ctx_create",
             "hdg_ctx_destroy", "hdg_last_error", "hdg_plan", "hdg_condense", "hdg_assemble_skeleton",
             "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
-            "hdg_launch_count", "hdg_debug_set_trace")
+            "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout")
 
 
 def _ptr(t):
@@ -265,20 +267,56 @@ class Context:
         return int(self._L.hdg_launch_count(self._h))
 
 
-def exchange(ctx: Context, send, recv, group=None):
-    """a7 transport: ship each rank's packed shared-face contributions to the owning ranks with
-    torch.distributed point-to-point ops (NCCL over NVLink on GPUs). Plumbing only — packing and the ordered
-    accumulation run in libhdg's kernels (hdg_assemble_skeleton / hdg_skeleton_accumulate)."""
+def exchange_layout(elem_face, face_elem, face_ndof, elem_ndof, rank_elem_begin, rank: int):
+    """a7 exchange layout of `rank`'s slab (hdg_exchange_layout: host only, no device or context needed).
+    Returns dict(send_counts, send_displs, recv_counts, recv_displs [nranks] int64, send_items, recv_items [n, 3]
+    int64) — see include/hdg.h for the packing."""
+    L = lib()
+    ef = np.ascontiguousarray(elem_face, dtype=np.int32)
+    fe = np.ascontiguousarray(face_elem, dtype=np.int32)
+    fn = np.ascontiguousarray(face_ndof, dtype=np.int32)
+    en = np.ascontiguousarray(elem_ndof, dtype=np.int32)
+    rb = np.ascontiguousarray(rank_elem_begin, dtype=np.int64)
+    nranks = len(rb) - 1
+    m = _Mesh(ef.shape[0], fe.shape[0], int(rb[rank]), int(rb[rank + 1] - rb[rank]), ef.ctypes.data, fe.ctypes.data,
+              fn.ctypes.data, en.ctypes.data, rb.ctypes.data)
+    arrs = [np.zeros(nranks, dtype=np.int64) for _ in range(4)]
+    ns, nr = ctypes.c_int64(), ctypes.c_int64()
+    P = ctypes.c_void_p
+    st = L.hdg_exchange_layout(ctypes.byref(m), rank, nranks, *[P(a.ctypes.data) for a in arrs], ctypes.byref(ns), None,
+                               ctypes.byref(nr), None)
+    if st != HDG_OK:
+        raise HDGError(st, "hdg_exchange_layout")
+    si = np.zeros((ns.value, 3), dtype=np.int64)
+    ri = np.zeros((nr.value, 3), dtype=np.int64)
+    st = L.hdg_exchange_layout(ctypes.byref(m), rank, nranks, *[P(a.ctypes.data) for a in arrs], ctypes.byref(ns),
+                               P(si.ctypes.data), ctypes.byref(nr), P(ri.ctypes.data))
+    if st != HDG_OK:
+        raise HDGError(st, "hdg_exchange_layout")
+    return dict(send_counts=arrs[0], send_displs=arrs[1], recv_counts=arrs[2], recv_displs=arrs[3], send_items=si,
+                recv_items=ri)
+
+
+def exchange_buffers(send, recv, send_counts, send_displs, recv_counts, recv_displs, rank: int, nranks: int,
+                     group=None):
+    """a7 transport: point-to-point torch.distributed ops moving each peer's slice of the packed send buffer to
+    it and filling recv (NCCL over NVLink for CUDA tensors; gloo for CPU tensors in the multi-process tests).
+    Plumbing only — packing and the ordered accumulation are libhdg kernels."""
     import torch.distributed as dist
-    sc, sd, rc, rd = ctx.exchange_counts()
     ops = []
-    for r in range(ctx.nranks):
-        if r == ctx.rank:
+    for r in range(nranks):
+        if r == rank:
             continue
-        if rc[r] > 0:
-            ops.append(dist.P2POp(dist.irecv, recv[rd[r]:rd[r] + rc[r]], r, group))
-        if sc[r] > 0:
-            ops.append(dist.P2POp(dist.isend, send[sd[r]:sd[r] + sc[r]], r, group))
+        if recv_counts[r] > 0:
+            ops.append(dist.P2POp(dist.irecv, recv[recv_displs[r]:recv_displs[r] + recv_counts[r]], r, group))
+        if send_counts[r] > 0:
+            ops.append(dist.P2POp(dist.isend, send[send_displs[r]:send_displs[r] + send_counts[r]], r, group))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
+
+
+def exchange(ctx: Context, send, recv, group=None):
+    """a7 transport for a planned context (counts from hdg_exchange_counts)."""
+    sc, sd, rc, rd = ctx.exchange_counts()
+    exchange_buffers(send, recv, sc, sd, rc, rd, ctx.rank, ctx.nranks, group)

@@ -70,6 +70,69 @@ bool force_sweep() {
   return v && strcmp(v, "sweep") == 0;
 }
 
+// a7 exchange layout of one rank's slab (host only, shared by hdg_plan and hdg_exchange_layout): for every face
+// slot of a local element whose face row is owned by another rank (its left element is remote), one send item
+// (face, local element, offset); for every owned face row whose right element is remote, one recv item (face,
+// global element, offset). Items are grouped by peer rank, then face id. Each item carries the face's g slice
+// and its n_fp x n_f strip of S_e: n_fp (1 + n_f) doubles.
+struct ExchangeLayout {
+  std::vector<int64_t> send_counts, send_displs, recv_counts, recv_displs, send_items, recv_items;
+  int64_t send_doubles = 0, recv_doubles = 0;
+};
+
+void build_exchange_layout(const hdg_mesh* m, int rank, int R, ExchangeLayout& x) {
+  const int64_t eb = m->elem_begin, n = m->n_elem, F = m->n_face;
+  x.send_counts.assign(R, 0); x.send_displs.assign(R, 0);
+  x.recv_counts.assign(R, 0); x.recv_displs.assign(R, 0);
+  auto rank_of = [&](int64_t e) {
+    return (int)(std::upper_bound(m->rank_elem_begin, m->rank_elem_begin + R + 1, e) - m->rank_elem_begin) - 1;
+  };
+  auto nf_of = [&](int64_t e) {
+    int t = 0;
+    for (int k = 0; k < 3; ++k) { const int32_t f = m->elem_face[3 * e + k]; if (f >= 0) t += m->face_ndof[f]; }
+    return t;
+  };
+  std::vector<std::tuple<int, int64_t, int64_t>> snd, rcv;   // (peer, face, element)
+  for (int64_t l = 0; l < n; ++l)
+    for (int k = 0; k < 3; ++k) {
+      const int32_t f = m->elem_face[3 * (eb + l) + k];
+      if (f < 0) continue;
+      const int32_t left = m->face_elem[2 * f];
+      if (left < eb || left >= eb + n) snd.emplace_back(rank_of(left), f, l);
+    }
+  for (int64_t f = 0; f < F; ++f) {
+    const int32_t left = m->face_elem[2 * f], r = m->face_elem[2 * f + 1];
+    if (left >= eb && left < eb + n && r >= 0 && (r < eb || r >= eb + n)) rcv.emplace_back(rank_of(r), f, r);
+  }
+  (void)rank;
+  std::sort(snd.begin(), snd.end());
+  std::sort(rcv.begin(), rcv.end());
+  int64_t o = 0;
+  for (auto& t : snd) {
+    const int peer = std::get<0>(t);
+    const int64_t f = std::get<1>(t), l = std::get<2>(t);
+    const int64_t sz = (int64_t)m->face_ndof[f] * (1 + nf_of(eb + l));
+    x.send_items.insert(x.send_items.end(), {f, l, o});
+    x.send_counts[peer] += sz;
+    o += sz;
+  }
+  x.send_doubles = o;
+  o = 0;
+  for (auto& t : rcv) {
+    const int peer = std::get<0>(t);
+    const int64_t f = std::get<1>(t), e = std::get<2>(t);
+    const int64_t sz = (int64_t)m->face_ndof[f] * (1 + nf_of(e));
+    x.recv_items.insert(x.recv_items.end(), {f, e, o});
+    x.recv_counts[peer] += sz;
+    o += sz;
+  }
+  x.recv_doubles = o;
+  for (int r = 1; r < R; ++r) {
+    x.send_displs[r] = x.send_displs[r - 1] + x.send_counts[r - 1];
+    x.recv_displs[r] = x.recv_displs[r - 1] + x.recv_counts[r - 1];
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -250,60 +313,19 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
 
   // ---- exchange lists (faces shared between slabs) ----------------------------------------------------------------
   const int R = ctx->nranks;
-  p.sk.send_counts.assign(R, 0); p.sk.send_displs.assign(R, 0);
-  p.sk.recv_counts.assign(R, 0); p.sk.recv_displs.assign(R, 0);
   if (R > 1) {
-    auto rank_of = [&](int64_t e) {
-      return (int)(std::upper_bound(m->rank_elem_begin, m->rank_elem_begin + R + 1, e) - m->rank_elem_begin) - 1;
-    };
-    auto nf_of = [&](int64_t e) {
-      int t = 0;
-      for (int k = 0; k < 3; ++k) { const int32_t f = m->elem_face[3 * e + k]; if (f >= 0) t += m->face_ndof[f]; }
-      return t;
-    };
-    std::vector<std::tuple<int, int64_t, int64_t>> snd, rcv;   // (peer, face, element)
-    for (int64_t l = 0; l < n; ++l)
-      for (int k = 0; k < 3; ++k) {
-        const int32_t f = m->elem_face[3 * (eb + l) + k];
-        if (f < 0) continue;
-        const int32_t left = m->face_elem[2 * f];
-        if (left < eb || left >= eb + n) snd.emplace_back(rank_of(left), f, l);
-      }
-    for (int64_t f = p.sk.f0; f < p.sk.f1; ++f) {
-      const int32_t r = m->face_elem[2 * f + 1];
-      if (r >= 0 && (r < eb || r >= eb + n)) rcv.emplace_back(rank_of(r), f, r);
-    }
-    std::sort(snd.begin(), snd.end());
-    std::sort(rcv.begin(), rcv.end());
-    std::vector<int64_t> si, ri;
-    int64_t o = 0;
-    for (auto& t : snd) {
-      const int peer = std::get<0>(t);
-      const int64_t f = std::get<1>(t), l = std::get<2>(t);
-      const int64_t sz = (int64_t)m->face_ndof[f] * (1 + nf[l]);
-      si.insert(si.end(), {f, l, o});
-      p.sk.send_counts[peer] += sz;
-      o += sz;
-    }
-    p.sk.send_doubles = o;
-    o = 0;
-    for (auto& t : rcv) {
-      const int peer = std::get<0>(t);
-      const int64_t f = std::get<1>(t), e = std::get<2>(t);
-      const int64_t sz = (int64_t)m->face_ndof[f] * (1 + nf_of(e));
-      ri.insert(ri.end(), {f, e, o});
-      p.sk.recv_counts[peer] += sz;
-      o += sz;
-    }
-    p.sk.recv_doubles = o;
-    for (int r = 1; r < R; ++r) {
-      p.sk.send_displs[r] = p.sk.send_displs[r - 1] + p.sk.send_counts[r - 1];
-      p.sk.recv_displs[r] = p.sk.recv_displs[r - 1] + p.sk.recv_counts[r - 1];
-    }
-    p.sk.n_send_items = (int64_t)snd.size();
-    p.sk.n_recv_items = (int64_t)rcv.size();
-    HDG_CUDA(ctx, upload(&p.sk.d_send_items, si.data(), si.size()));
-    HDG_CUDA(ctx, upload(&p.sk.d_recv_items, ri.data(), ri.size()));
+    ExchangeLayout x;
+    build_exchange_layout(m, ctx->rank, R, x);
+    p.sk.send_counts = x.send_counts; p.sk.send_displs = x.send_displs;
+    p.sk.recv_counts = x.recv_counts; p.sk.recv_displs = x.recv_displs;
+    p.sk.send_doubles = x.send_doubles; p.sk.recv_doubles = x.recv_doubles;
+    p.sk.n_send_items = (int64_t)x.send_items.size() / 3;
+    p.sk.n_recv_items = (int64_t)x.recv_items.size() / 3;
+    HDG_CUDA(ctx, upload(&p.sk.d_send_items, x.send_items.data(), x.send_items.size()));
+    HDG_CUDA(ctx, upload(&p.sk.d_recv_items, x.recv_items.data(), x.recv_items.size()));
+  } else {
+    p.sk.send_counts.assign(1, 0); p.sk.send_displs.assign(1, 0);
+    p.sk.recv_counts.assign(1, 0); p.sk.recv_displs.assign(1, 0);
   }
 
   p.valid = true;
@@ -449,6 +471,30 @@ hdg_status hdg_first_error(hdg_ctx ctx, const int32_t* info, int64_t* elem, int3
   if (cudaMemcpy(code, info + h, sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(ctx, HDG_ERR_CUDA, "hdg_first_error: copy");
   return fail(ctx, HDG_ERR_SINGULAR, "singular local block: element %lld (info %d)", (long long)(p.eb + h), *code);
+}
+
+hdg_status hdg_exchange_layout(const hdg_mesh* m, int rank, int nranks, int64_t* send_counts, int64_t* send_displs,
+                               int64_t* recv_counts, int64_t* recv_displs, int64_t* n_send_items, int64_t* send_items,
+                               int64_t* n_recv_items, int64_t* recv_items) {
+  if (!m || !m->elem_face || !m->face_elem || !m->face_ndof || !m->rank_elem_begin || nranks < 1 || rank < 0 ||
+      rank >= nranks || !n_send_items || !n_recv_items)
+    return HDG_ERR_ARG;
+  if (m->rank_elem_begin[rank] != m->elem_begin || m->rank_elem_begin[rank + 1] != m->elem_begin + m->n_elem)
+    return HDG_ERR_ARG;
+  ExchangeLayout x;
+  build_exchange_layout(m, rank, nranks, x);
+  for (int r = 0; r < nranks; ++r) {
+    if (send_counts) send_counts[r] = x.send_counts[r];
+    if (send_displs) send_displs[r] = x.send_displs[r];
+    if (recv_counts) recv_counts[r] = x.recv_counts[r];
+    if (recv_displs) recv_displs[r] = x.recv_displs[r];
+  }
+  const int64_t ns = (int64_t)x.send_items.size() / 3, nr = (int64_t)x.recv_items.size() / 3;
+  if (send_items) std::copy(x.send_items.begin(), x.send_items.end(), send_items);
+  if (recv_items) std::copy(x.recv_items.begin(), x.recv_items.end(), recv_items);
+  *n_send_items = ns;
+  *n_recv_items = nr;
+  return HDG_OK;
 }
 
 }  // extern "C"
