@@ -35,7 +35,7 @@
 namespace hdg {
 namespace {
 
-constexpr int NB = 16;    // panel width
+constexpr int NB = kSweepNB;   // panel width (see diag_block for NB = 8 / 16)
 
 // instrumentation (hdg_debug_set_trace): clock64 stamp k of element-iteration it, CTA 0, warps 0 and 1
 #define SW_STAMP(it, k)                                                                                       \
@@ -72,7 +72,7 @@ __device__ __forceinline__ bool pivot_bad(double x) {
 // with L^-1 and U^-1 (8x8, row stride LDI) into Li8 / Ui8. Lanes 0..7: row r of [block | I]; lanes 8..15: row r of
 // U^-1 by the forward recurrence (see diag_chain); lanes 16..31 ride along with zero coefficients. Step c
 // broadcasts 8-c + c+1 = 9 values (half of a 16-wide step). Writes L\U rows < nbv back to X and to LU.
-__device__ __forceinline__ bool lu8(double* X, int ld, int r0, int nbv, double* Li8, double* Ui8, double* LU, int ne,
+__device__ __noinline__ bool lu8(double* X, int ld, int r0, int nbv, double* Li8, double* Ui8, double* LU, int ne,
                                     int lane) {
   const int r = lane & 7;
   const bool lo = lane < 8, up = lane >= 8 && lane < 16;
@@ -210,6 +210,18 @@ __device__ __forceinline__ bool diag_chain(double* T, int ldT, int jb, int nb, d
   st8(Uinv + 8, LDI, Y, lane);
   __syncwarp();
   return __any_sync(0xffffffffu, viol);
+}
+
+// The diagonal block of one panel: NB = 8 -> one 8x8 LU (its L^-1, U^-1 written straight into the Linv / Uinv
+// buffers); NB = 16 -> the two-LU form above.
+__device__ __forceinline__ bool diag_block(double* T, int ldT, int jb, int nb, double* Linv, double* Uinv,
+                                           double* scratch, double* LU, int ne, int lane) {
+  if constexpr (NB == 8) {
+    __syncwarp();
+    return lu8(T, ldT, jb, nb, Linv, Uinv, LU, ne, lane);
+  } else {
+    return diag_chain(T, ldT, jb, nb, Linv, Uinv, scratch, LU, ne, lane);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------------------
@@ -670,7 +682,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           SW_STAMP(tit, 10 + 4 * p);
         }
         if (do_diag)
-          viol |= diag_chain(T, ldT, jd, nd, Linv_b + dbuf * NB * LDI, Uinv_b + dbuf * NB * LDI, bcast, LUd, ne, lane);
+          viol |= diag_block(T, ldT, jd, nd, Linv_b + dbuf * NB * LDI, Uinv_b + dbuf * NB * LDI, bcast, LUd, ne, lane);
         if (p < 0) {
           SW_STAMP(tit, 2);
           mbar_wait(&mbar[1], ph);

@@ -37,10 +37,11 @@ __global__ void bench(double* LUg, long long* cyc, int nwarps_busy) {
 }}
 int main() {
   double* LUg; long long* cyc; cudaMalloc(&LUg, 120 * 120 * 8); cudaMalloc(&cyc, 64);
-  cudaFuncSetAttribute(hdg::bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
-  for (int nw : {1, 8}) {
-    hdg::bench<<<1, 32 * nw, 200000>>>(LUg, cyc, nw); cudaDeviceSynchronize();
+  cudaFuncSetAttribute(hdg::bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  for (int smem : {232448, 225000, 215000, 200000, 190000}) {
+    // the carveout: the shared-memory size sets how much of the unified L1 is left
+    hdg::bench<<<1, 32, smem>>>(LUg, cyc, 1); cudaDeviceSynchronize();
     long long h[4]; cudaMemcpy(h, cyc, 32, cudaMemcpyDeviceToHost);
-    printf("%d warps (chain = last): prep %lld | update %lld | diag %lld  (viol %lld, %s)\n", nw, h[0], h[1], h[2], h[3], cudaGetErrorString(cudaGetLastError()));
+    printf("smem %6d B: prep %lld | update %lld | diag %lld  (viol %lld, %s)\n", smem, h[0], h[1], h[2], h[3], cudaGetErrorString(cudaGetLastError()));
   }
 }
