@@ -87,7 +87,8 @@ def main():
     if a.launches:
         tot, cnt = launches(a.launches)
         path = os.path.join(PROF, f"{a.tag}_launches_{a.launch_config}.md")
-        hot = [k for k in tot if any(s in k for s in ("condense_kernel", "assemble", "backsub", "pack", "accumulate"))]
+        hot = [k for k in tot if any(s in k for s in ("condense_kernel", "sweep_kernel", "assemble", "backsub", "pack",
+                                                       "accumulate"))]
         step = sum(tot[k] / max(1, cnt[k]) for k in hot)
         with open(path, "w") as f:
             f.write(f"# {a.tag} launch list — `bench.py --config {a.launch_config}` under "
@@ -105,7 +106,8 @@ def main():
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for rep, cfg in zip(a.rep, a.config):
         m, kname = raw_metrics(rep)
-        short = "condense" if "condense" in kname else ("backsub" if "backsub" in kname else kname.split("(")[0][-30:])
+        short = ("condense_sweep" if "sweep_kernel" in kname else "condense" if "condense" in kname else
+                 "backsub" if "backsub" in kname else "".join(ch for ch in kname.split("(")[0][-30:] if ch.isalnum()))
         path = os.path.join(PROF, f"{a.tag}_{short}_{cfg}_ncu.md")
         with open(path, "w") as f:
             f.write(f"# {a.tag} — `ncu --set full --clock-control none --import-source on` of `{kname[:100]}` "
@@ -114,7 +116,7 @@ def main():
                 if key in m:
                     f.write(f"| {label} (`{key}`) | {m[key][0]} | {m[key][1]} |\n")
             f.write("\nWarp-stall samples by source line (tools/ncu_hot.py):\n\n```\n" + hot_lines(rep) + "```\n")
-        if "dram__bytes_read.sum" in m and short == "condense":
+        if "dram__bytes_read.sum" in m and short.startswith("condense"):
             rd = to_bytes(*m["dram__bytes_read.sum"])
             wr = to_bytes(*m["dram__bytes_write.sum"])
             traffic[cfg] = rd + wr
