@@ -658,12 +658,13 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           if (__syncthreads_or(viol)) { aborted = true; break; }
           SW_STAMP(tit, 8 + 4 * p);
           viol = false;
-          if (has_next)
-            viol |= prep_next(T, ldT, jb, nb, jn, nextr_hi, nn8, Linv_b + buf * NB * LDI, Uinv_b + buf * NB * LDI, LU,
-                              ne, lane);
+          (void)buf;
           named_arrive(1, THREADS);
           SW_STAMP(tit, 9 + 4 * p);
           if (has_next) {
+            // the next block's L21 rows / U12 columns come from MMA workers 0 and 1 (their first jobs, off the
+            // chain warp's critical path); wait for just those two tiles
+            named_sync(2, 96);
             upd_block(T, ldT, T + jb, ldT, T + (size_t)jb * ldT, ldT, jn, nn8 >> 3, jn, nn8 >> 3, nk, lane);
             __syncwarp();
             jd = jn;
@@ -797,6 +798,13 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           const int cU0 = has_next ? jn + nn8 : jb + nb8;           // columns [cU0, NC)
           const int tA = (RA - rA0) >> 3, tC = G.NF8 >> 3, tU = (NC - cU0) >> 3;
           const int nA = (tA + 1) >> 1, nCt = (tC + 1) >> 1, nU = (tU + 1) >> 1;
+          if (has_next && w < 2) {
+            // the tiles the chain warp's next diagonal block needs, first: L21 of its rows, U12 of its columns
+            if (w == 0) viol |= trsm_right(T, ldT, jn, (nextr_hi - jn) >> 3, jb, nb, Uinv, ne, LU, lane);
+            else trsm_left(T, ldT, jb, nb, Linv, jn, nn8 >> 3, LU, ne, lane);
+            __syncwarp();
+            named_arrive(2, 96);
+          }
           for (int job = (a.debug & 1) ? 1 << 30 : w; job < nA + nCt + nU; job += NWK) {
             if (job < nA) {
               viol |= trsm_right(T, ldT, rA0 + 16 * job, min(2, tA - 2 * job), jb, nb, Uinv, ne, LU, lane);
