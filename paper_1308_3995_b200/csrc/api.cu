@@ -271,9 +271,11 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     B.count = (int64_t)b.second.size();
     const Geo geo(B.ne, B.nf);
     B.t_in_smem = geo.smem_bytes(true) <= (int64_t)ctx->smem_optin;
-    // the sweep kernel (one element per SM, chain warp + MMA workers) wins from n_e ~ 96 up (C4: 46 vs 57 ms);
-    // below, the panel kernel with several CTAs per SM is faster (C3: 34 vs 47 ms) — measured on the box
-    B.sweep = sweep_supported(B.ne, B.nf, ctx->smem_optin) && !force_panel() && (B.ne >= 96 || force_sweep());
+    // measured on the box: the sweep kernel (chain warp + MMA workers; 2 CTAs per SM when they fit) wins for
+    // n_e >= 96 (C4: 45 vs 57 ms) and n_e <= 32 (C2: 0.82 vs 0.95 ms); the panel kernel for n_e in between
+    // (C3: 34 vs 40 ms)
+    B.sweep = sweep_supported(B.ne, B.nf, ctx->smem_optin) && !force_panel() &&
+              (B.ne >= 96 || B.ne <= 32 || force_sweep());
     if (!B.sweep && !B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
     if (B.sweep) {   // exact-path slab per resident CTA (at most 2 per SM)
       const SweepGeo sg(B.ne, B.nf);

@@ -72,8 +72,9 @@ __device__ __forceinline__ bool pivot_bad(double x) {
 // with L^-1 and U^-1 (8x8, row stride LDI) into Li8 / Ui8. Lanes 0..7: row r of [block | I]; lanes 8..15: row r of
 // U^-1 by the forward recurrence (see diag_chain); lanes 16..31 ride along with zero coefficients. Step c
 // broadcasts 8-c + c+1 = 9 values (half of a 16-wide step). Writes L\U rows < nbv back to X and to LU.
-__device__ __noinline__ bool lu8(double* X, int ld, int r0, int nbv, double* Li8, double* Ui8, double* LU, int ne,
+__device__ __forceinline__ bool lu8(double* X, int ld, int r0, int nbv, double* Li8, double* Ui8, double* LU, int ne,
                                     int lane) {
+  __syncwarp();
   const int r = lane & 7;
   const bool lo = lane < 8, up = lane >= 8 && lane < 16;
   double d[8], e[8];
@@ -938,6 +939,14 @@ cudaError_t launch_condense_sweep(const CondenseArgs& a, int sms, size_t smem_op
   const SweepGeo G(a.ne, a.nf);
   (void)smem_optin;
   const int slots = (G.ntiles + 5) / 6;
+  // two CTAs (two elements, two chain warps) per SM when their shared memory fits: the 128-register build has no
+  // spills up to 12 [S|g] slots (checked with -Xptxas -v), and the second element hides the first's chain latency
+  const bool two = 2 * (G.smem_bytes() + 1024) <= 233472 && slots <= 12;
+  if (two) {
+    if (slots <= 4) return launch_sweep_t<8, 4, 2>(a, sms, s);
+    if (slots <= 7) return launch_sweep_t<8, 7, 2>(a, sms, s);
+    return launch_sweep_t<8, 12, 2>(a, sms, s);
+  }
   if (slots <= 4) return launch_sweep_t<8, 4, 1>(a, sms, s);
   if (slots <= 7) return launch_sweep_t<8, 7, 1>(a, sms, s);
   if (slots <= 11) return launch_sweep_t<8, 11, 1>(a, sms, s);
