@@ -274,9 +274,14 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     // measured on the box: the sweep kernel (chain warp + MMA workers; 2 CTAs per SM when they fit) wins for
     // n_e >= 96 (C4: 45 vs 57 ms) and n_e <= 32 (C2: 0.82 vs 0.95 ms); the panel kernel for n_e in between
     // (C3: 34 vs 40 ms)
-    B.sweep = sweep_supported(B.ne, B.nf, ctx->smem_optin) && !force_panel() &&
-              (B.ne >= 96 || B.ne <= 32 || force_sweep());
-    if (!B.sweep && !B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
+    const char* forced = getenv("HDG_CONDENSE_KERNEL");
+    const std::string fk = forced ? forced : "";
+    // the warp-per-element kernel is correct (parity-tested) but measured slower than the sweep kernel on C2
+    // (1.03 vs 0.82 ms): opt-in only
+    B.warp = warp_supported(B.ne, B.nf) && fk == "warp";
+    B.sweep = !B.warp && sweep_supported(B.ne, B.nf, ctx->smem_optin) && fk != "panel" &&
+              (B.ne >= 96 || B.ne <= 32 || fk == "sweep");
+    if (!B.warp && !B.sweep && !B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
     if (B.sweep) {   // exact-path slab per resident CTA (at most 2 per SM)
       const SweepGeo sg(B.ne, B.nf);
       scratch = std::max(scratch, ((int64_t)sg.RA * sg.ldT + (int64_t)sg.NF8 * sg.ldC) * 2 * ctx->sms);
@@ -373,7 +378,8 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
     a.scratch = p.d_scratch;
     a.trace = ctx->trace;
     a.debug = getenv("HDG_DEBUG_MODE") ? atoi(getenv("HDG_DEBUG_MODE")) : 0;
-    if (b.sweep) HDG_CUDA(ctx, launch_condense_sweep(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
+    if (b.warp) HDG_CUDA(ctx, launch_condense_warp(a, ctx->sms, s, &ctx->launches));
+    else if (b.sweep) HDG_CUDA(ctx, launch_condense_sweep(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
     else HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
   }
   return HDG_OK;

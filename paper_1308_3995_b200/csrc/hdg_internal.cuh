@@ -105,6 +105,7 @@ struct Bucket {
   int32_t* d_elems;   // device list of local element ids
   bool t_in_smem;     // panel kernel: working matrix in shared memory (else global scratch)
   bool sweep;         // condensed by the sweep kernel (condense_sweep.cu)
+  bool warp;          // condensed by the warp-per-element kernel (condense_warp.cu)
 };
 
 // Skeleton assembly data (owned rows).
@@ -158,6 +159,8 @@ struct hdg_ctx_s {
 namespace hdg {
 cudaError_t launch_condense(const CondenseArgs& a, bool t_in_smem, int sms, cudaStream_t s, int64_t* launches);
 bool sweep_supported(int ne, int nf, size_t smem_optin);
+bool warp_supported(int ne, int nf);
+cudaError_t launch_condense_warp(const CondenseArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_condense_sweep(const CondenseArgs& a, int sms, size_t smem_optin, cudaStream_t s, int64_t* launches);
 cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s);

@@ -240,7 +240,7 @@ def test_device_generator_bit_identical(cuda):
     assert [hex(x) for x in raw[1]] == ["0x408f276d", "0x41c83b0e", "0xa20bc7c6", "0x6d5451fd"]
 
 
-@pytest.fixture(params=["sweep", "panel"])
+@pytest.fixture(params=["sweep", "panel", "warp"])
 def kernel(request, monkeypatch):
     """Force one condensation kernel for every bucket it supports (read by hdg_plan)."""
     monkeypatch.setenv("HDG_CONDENSE_KERNEL", request.param)
@@ -254,7 +254,7 @@ def test_both_condense_kernels(cuda, kernel, name, nr, nt):
     check_all(gen.config(name, nr=nr, nt=nt))
 
 
-@pytest.mark.parametrize("name", ["C3", "C4"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_both_kernels_pivot_forcing(cuda, kernel, name):
     """P9 on both kernels: permuted rows force the exact (pivoting) path; a zero-ish leading entry too."""
     w = gen.config(name, nr=2, nt=4)
