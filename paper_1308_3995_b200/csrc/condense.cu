@@ -655,7 +655,13 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
     // ---- a5 factors: L\U row-major + row permutation ---------------------------------------------------------
     {
       double* LU = reinterpret_cast<double*>(a.factors + a.offF[l]);
-      for (int idx = tid; idx < ne * ne; idx += THREADS) LU[idx] = T[(idx / ne) * ldT + idx % ne];
+      // one warp per row, lanes over column pairs: coalesced 16-byte loads and stores, no index division
+      // (ne and ldT are even, so every row start is 16-byte aligned in T and in the record)
+      for (int i = warp; i < ne; i += NWARPS) {
+        const double2* src = reinterpret_cast<const double2*>(T + (size_t)i * ldT);
+        double2* dst = reinterpret_cast<double2*>(LU + (size_t)i * ne);
+        for (int j = lane; j < (ne >> 1); j += 32) dst[j] = src[j];
+      }
       // row permutation of P A: follow where original row i ends up through the interchanges (parallel in i)
       int32_t* perm = reinterpret_cast<int32_t*>(LU + (int64_t)ne * ne);
       for (int i = tid; i < ne; i += THREADS) {
