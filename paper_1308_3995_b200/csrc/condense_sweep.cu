@@ -420,6 +420,43 @@ __device__ __forceinline__ void upd_block(double* dst, int ldd, const double* Ap
             make_double2(acc[i][j][0], acc[i][j][1]);
 }
 
+// Full 16x32 block, k = 16: every fragment (2 x 4 A, 4 x 4 B) is loaded before the first MMA, so the 24 shared
+// loads issue back to back and the 32 MMAs (8 independent accumulator chains) follow without load stalls.
+__device__ __forceinline__ void upd_full16(double* dst, int ldd, const double* Ap, int lda, const double* Bp, int ldb,
+                                           int r0, int c0, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  double a[4][2], b[4][4];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    a[kk][0] = -Ap[(size_t)(r0 + gid) * lda + 4 * kk + tig];
+    a[kk][1] = -Ap[(size_t)(r0 + 8 + gid) * lda + 4 * kk + tig];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[kk][j] = Bp[(size_t)(4 * kk + tig) * ldb + c0 + 8 * j + gid];
+  }
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2 v = *reinterpret_cast<const double2*>(dst + (size_t)(r0 + 8 * i + gid) * ldd + c0 + 8 * j + 2 * tig);
+      acc[i][j][0] = v.x;
+      acc[i][j][1] = v.y;
+    }
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      dmma(acc[0][j], a[kk][0], b[kk][j]);
+      dmma(acc[1][j], a[kk][1], b[kk][j]);
+    }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<double2*>(dst + (size_t)(r0 + 8 * i + gid) * ldd + c0 + 8 * j + 2 * tig) =
+          make_double2(acc[i][j][0], acc[i][j][1]);
+}
+
 // A rectangular trailing region [r_lo, r_hi) x [c_lo, c_hi) cut into 16x32 blocks (row remainder 8, column
 // remainder 8/16/24); block index -> geometry.
 struct Region {
@@ -851,7 +888,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
               const int br = bi / nbc, bc = bi - br * nbc;
               const int r0 = r_lo + 16 * br, c0 = c_lo + 32 * bc;
               const int nrt = min(2, (r_hi - r0) >> 3), nct = min(4, (c_hi - c0) >> 3);
-              if (nrt == 2 && nct == 4) upd_block(dst, ldd, dst + jb, ldd, T + (size_t)jb * ldT, ldT, r0, 2, c0, 4, nk, lane);
+              if (nrt == 2 && nct == 4 && NBC == NB) upd_full16(dst, ldd, dst + jb, ldd, T + (size_t)jb * ldT, ldT, r0, c0, lane);
+              else if (nrt == 2 && nct == 4) upd_block(dst, ldd, dst + jb, ldd, T + (size_t)jb * ldT, ldT, r0, 2, c0, 4, nk, lane);
               else upd_block(dst, ldd, dst + jb, ldd, T + (size_t)jb * ldT, ldT, r0, nrt, c0, nct, nk, lane);
             }
           }
