@@ -807,15 +807,11 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         if (__syncthreads_or(viol)) { aborted = true; p_ab = p; break; }
         SW_STAMP(tit, 8 + 4 * p);
         viol = false;
-        if (helper) {
+        if (helper && p >= 1 && ln >= 0) {
           // the rows of panel p-1 are dead: stream the next element's rows in
-          if (p >= 1 && ln >= 0) {
-            if (p == 1) expect_all();
-            fence_proxy_async();
-            load_rows(ln, (p - 1) * NB, p * NB);
-          }
-          named_arrive(1, THREADS);
-          continue;
+          if (p == 1) expect_all();
+          fence_proxy_async();
+          load_rows(ln, (p - 1) * NB, p * NB);
         }
         // one panel step; NBC = 16: a full panel, every size below is a compile-time constant (no guards around
         // the fragment loads, so they are scheduled ahead of the DMMAs); NBC = 0: the partial last panel
@@ -836,14 +832,14 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           const int cU0 = has_next ? jn + nn8 : jb + nb8;           // columns [cU0, NC)
           const int tA = (RA - rA0) >> 3, tC = G.NF8 >> 3, tU = (NC - cU0) >> 3;
           const int nA = (tA + 1) >> 1, nCt = (tC + 1) >> 1, nU = (tU + 1) >> 1;
-          if (has_next && w < 2) {
+          if (has_next && w < 2 && !helper) {
             // the tiles the chain warp's next diagonal block needs, first: L21 of its rows, U12 of its columns
             if (w == 0) viol |= trsm_right(T, ldT, jn, (nextr_hi - jn) >> 3, jb, nb, Uinv, ne, LU, lane);
             else trsm_left(T, ldT, jb, nb, Linv, jn, nn8 >> 3, LU, ne, lane);
             __syncwarp();
             named_arrive(2, 96);
           }
-          for (int job = (a.debug & 1) ? 1 << 30 : w; job < nA + nCt + nU; job += NWK) {
+          for (int job = ((a.debug & 1) || helper) ? 1 << 30 : w; job < nA + nCt + nU; job += NWK) {
             if (job < nA) {
               viol |= trsm_right(T, ldT, rA0 + 16 * job, min(2, tA - 2 * job), jb, nb, Uinv, ne, LU, lane);
             } else if (job < nA + nCt) {
@@ -857,7 +853,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           named_sync(1, THREADS);
           SW_STAMP(tit, 9 + 4 * p);
           // ---- register-resident [S | g] -= Y_p W_p
-          {
+          if (!helper) {
             const double* Yp = Cr + jb;
             const double* Wp = T + (size_t)jb * ldT;
 #pragma unroll
@@ -876,7 +872,12 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
             const Region R1b(nextr_hi, RA, jn, NC);
             const Region R2(0, G.NF8, jn, CB);
             const int tot = R1a.nblk + R1b.nblk + R2.nblk;
-            for (int b = (a.debug & 1) ? 1 << 30 : w; b < tot; b += NWK) {
+            // trailing blocks: the 6 MMA workers, plus the helper in the first half of the panels (there the
+            // workers bound the step; later the chain warp does, and it shares the helper's SMSP tensor pipe)
+            const bool hjoin = 2 * p < G.npan;
+            const int nt_w = hjoin ? NWK + 1 : NWK;
+            const int tw = helper ? (hjoin ? NWK : 1 << 30) : w;
+            for (int b = (a.debug & 1) ? 1 << 30 : tw; b < tot; b += nt_w) {
               // region selection with plain integers (no addresses of locals: they would live on the stack)
               int bi = b, r_lo, r_hi, c_lo, c_hi, nbc;
               const bool inC = bi >= R1a.nblk + R1b.nblk;
