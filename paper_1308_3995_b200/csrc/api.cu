@@ -281,8 +281,10 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     B.warp = warp_supported(B.ne, B.nf) && fk == "warp";
     B.sweep = !B.warp && sweep_supported(B.ne, B.nf, ctx->smem_optin) && fk != "panel" &&
               (B.ne >= 96 || B.ne <= 32 || fk == "sweep");
-    if (!B.warp && !B.sweep && !B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
-    if (B.sweep) {   // exact-path slab per resident CTA (at most 2 per SM)
+    // elements larger than one SM (C5's n_e = 180, 252): the sweep kernel on an L2-resident global slab
+    B.sweep_gt = !B.warp && !B.sweep && !B.t_in_smem && fk != "panel" && sweep_gt_supported(B.ne, B.nf);
+    if (!B.warp && !B.sweep && !B.sweep_gt && !B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
+    if (B.sweep || B.sweep_gt) {   // exact-path (and GT working) slab per resident CTA (at most 2 per SM)
       const SweepGeo sg(B.ne, B.nf);
       scratch = std::max(scratch, ((int64_t)sg.RA * sg.ldT + (int64_t)sg.NF8 * sg.ldC) * 2 * ctx->sms);
     }
@@ -380,6 +382,7 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
     a.debug = getenv("HDG_DEBUG_MODE") ? atoi(getenv("HDG_DEBUG_MODE")) : 0;
     if (b.warp) HDG_CUDA(ctx, launch_condense_warp(a, ctx->sms, s, &ctx->launches));
     else if (b.sweep) HDG_CUDA(ctx, launch_condense_sweep(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
+    else if (b.sweep_gt) HDG_CUDA(ctx, launch_condense_sweep_gt(a, ctx->sms, s, &ctx->launches));
     else HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
   }
   return HDG_OK;

@@ -27,6 +27,7 @@
 // Data movement: TMA bulk copies (cp.async.bulk + mbarrier transaction counts) stage A_e rows, B_e rows and C_e
 // rows; the L\U rows of each finished panel leave by TMA bulk stores (shared -> global) while the sweep goes on;
 // the next element's blocks are prefetched into L2 at the start of the current one.
+#include <algorithm>
 #include <type_traits>
 
 #include "dev_common.cuh"
@@ -599,7 +600,11 @@ __device__ __noinline__ void exact_element(const double* A, const double* Bm, co
 //   * the chain warp factors the next element's first diagonal block while the workers finish the current
 //     element's last panel and store [S | g].
 //   * Linv/Uinv buffers alternate on a panel counter that runs across elements.
-template <int NWARPS, int MAXT, int MINB>
+// GT = true: the working matrix T and the C rows live in this CTA's slab of global scratch (L2-resident) instead of
+// shared memory — for elements whose working set exceeds one SM (C5's n_e = 180, 252 buckets). The element's rows
+// are then copied in by all threads at its start (no TMA pipeline, no early prologue); everything else is the same
+// code on generic pointers.
+template <int NWARPS, int MAXT, int MINB, bool GT>
 __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const CondenseArgs a) {
   constexpr int THREADS = NWARPS * 32;
   constexpr int CW = NWARPS - 1;   // the chain warp: the highest warp id wins issue arbitration in its SMSP
@@ -613,17 +618,17 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
   const int gid = lane >> 2, tig = lane & 3;
   const int r1 = ne < NB ? ne : NB;
 
-  double* T = smem;
+  double* X = a.scratch + (size_t)blockIdx.x * (size_t)(G.RA * ldT + G.NF8 * ldC);   // exact-path slab
+  double* T = GT ? X : smem;
   double* Cr = T + (size_t)RA * ldT;
-  double* Linv_b = Cr + (size_t)G.NF8 * ldC;       // [2][NB * LDI]
+  double* Linv_b = GT ? smem : Cr + (size_t)G.NF8 * ldC;       // [2][NB * LDI]
   double* Uinv_b = Linv_b + 2 * NB * LDI;          // [2][NB * LDI]
   double* bcast = Uinv_b + 2 * NB * LDI;           // [2][BCW] (spare)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(bcast + 2 * BCW);   // [0] A rows < 16, [1] everything else
   int* piv = reinterpret_cast<int*>(mbar + 4);
   int* sfail = piv + RA;
-  double* X = a.scratch + (size_t)blockIdx.x * (size_t)(G.RA * ldT + G.NF8 * ldC);   // exact-path slab
 
-  for (int i = tid; i < RA * ldT + G.NF8 * ldC; i += THREADS) smem[i] = 0.0;
+  for (int i = tid; i < RA * ldT + G.NF8 * ldC; i += THREADS) T[i] = 0.0;
   if (tid == 0) {
     mbar_init(&mbar[0]);
     mbar_init(&mbar[1]);
@@ -653,6 +658,25 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     const double* Cm = a.C + a.offC[l];
     for (int i = lane; i < nf; i += 32) bulk_g2s(Cr + (size_t)i * ldC, Cm + (size_t)i * ne, (uint32_t)(ne * 8), &mbar[1]);
   };
+  // GT: all threads copy element l's A, B, C rows into the global working slab (16-byte vectors)
+  auto stage_global = [&](int64_t l) {
+    const double2* A = reinterpret_cast<const double2*>(a.A + a.offA[l]);
+    const double2* Bm = reinterpret_cast<const double2*>(a.B + a.offB[l]);
+    const double2* Cm = reinterpret_cast<const double2*>(a.C + a.offC[l]);
+    const int ha = ne >> 1, hf = nf >> 1;
+    for (int q = tid; q < ne * ha; q += THREADS) {
+      const int i = q / ha, j = q - i * ha;
+      *reinterpret_cast<double2*>(T + (size_t)i * ldT + 2 * j) = __ldg(A + q);
+    }
+    for (int q = tid; q < ne * hf; q += THREADS) {
+      const int i = q / hf, j = q - i * hf;
+      *reinterpret_cast<double2*>(T + (size_t)i * ldT + CB + 2 * j) = __ldg(Bm + q);
+    }
+    for (int q = tid; q < nf * ha; q += THREADS) {
+      const int i = q / ha, j = q - i * ha;
+      *reinterpret_cast<double2*>(Cr + (size_t)i * ldC + 2 * j) = __ldg(Cm + q);
+    }
+  };
   auto prefetch = [&](int64_t l) {
     prefetch_l2(a.A + a.offA[l], (uint32_t)(ne * ne * 8));
     prefetch_l2(a.B + a.offB[l], (uint32_t)(ne * nf * 8));
@@ -660,7 +684,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     prefetch_l2(a.D + a.offD[l], (uint32_t)(nf * nf * 8));
   };
 
-  if (blockIdx.x < a.count && warp == 0) {
+  if (!GT && blockIdx.x < a.count && warp == 0) {
     expect_all();
     load_rows(elem_of(blockIdx.x), 0, ne);
     load_C(elem_of(blockIdx.x));
@@ -679,6 +703,10 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       const int64_t tit = (it - blockIdx.x) / gridDim.x;
       SW_STAMP(tit, 0);
       double* LU = reinterpret_cast<double*>(a.factors + a.offF[l]);
+      if constexpr (GT) {
+        stage_global(l);
+        __syncthreads();   // G: the element is in the global working slab
+      }
       bool aborted = false, early = false;
       for (int p = need_pro ? -1 : 0; p < G.npan; ++p) {
         const int jb = p * NB, nb = min(NB, ne - jb), nk = (nb + 3) & ~3;
@@ -691,7 +719,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         double* LUd = LU;
         bool do_diag = true;
         if (p < 0) {
-          mbar_wait(&mbar[0], ph);
+          if (!GT) mbar_wait(&mbar[0], ph);
         } else {
           if (__syncthreads_or(viol)) { aborted = true; break; }
           SW_STAMP(tit, 8 + 4 * p);
@@ -708,7 +736,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
             jd = jn;
             nd = nn;
             dbuf = buf ^ 1;
-          } else if (next < a.count && G.npan >= 2) {
+          } else if (!GT && next < a.count && G.npan >= 2) {
             // the next element's first diagonal block, overlapped with the workers' last-panel work
             // (npan == 1: its rows arrive only after barrier F)
             mbar_wait(&mbar[0], ph ^ 1u);
@@ -724,7 +752,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           viol |= diag_block(T, ldT, jd, nd, Linv_b + dbuf * NB * LDI, Uinv_b + dbuf * NB * LDI, bcast, LUd, ne, lane);
         if (p < 0) {
           SW_STAMP(tit, 2);
-          mbar_wait(&mbar[1], ph);
+          if (!GT) mbar_wait(&mbar[1], ph);
           SW_STAMP(tit, 3);
         } else {
           SW_STAMP(tit, 11 + 4 * p);
@@ -778,6 +806,10 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       const int64_t tit = (it - blockIdx.x) / gridDim.x;
       SW_STAMP(tit, 0);
       double* LU = reinterpret_cast<double*>(a.factors + a.offF[l]);
+      if constexpr (GT) {
+        stage_global(l);
+        __syncthreads();   // G
+      }
       if (helper) {
         if (lane == 0 && ln >= 0) prefetch(ln);
         const double* re = a.re + a.offRe[l];
@@ -796,9 +828,9 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         }
       }
       SW_STAMP(tit, 4);
-      mbar_wait(&mbar[0], ph);
+      if (!GT) mbar_wait(&mbar[0], ph);
       SW_STAMP(tit, 5);
-      mbar_wait(&mbar[1], ph);
+      if (!GT) mbar_wait(&mbar[1], ph);
       SW_STAMP(tit, 3);
       bool viol = false;
       bool aborted = false;
@@ -807,7 +839,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         if (__syncthreads_or(viol)) { aborted = true; p_ab = p; break; }
         SW_STAMP(tit, 8 + 4 * p);
         viol = false;
-        if (helper && p >= 1 && ln >= 0) {
+        if (!GT && helper && p >= 1 && ln >= 0) {
           // the rows of panel p-1 are dead: stream the next element's rows in
           if (p == 1) expect_all();
           fence_proxy_async();
@@ -904,7 +936,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         ++pc;
         // issue every load of the next element that is not in flight yet (its rows of T are dead), then redo
         // this element on the exact path in global scratch
-        if (ln >= 0 && helper) {
+        if (!GT && ln >= 0 && helper) {
           if (p_ab <= 1) expect_all();
           fence_proxy_async();
           load_rows(ln, p_ab >= 1 ? (p_ab - 1) * NB : 0, ne);
@@ -933,7 +965,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         SW_STAMP(tit, 6);
         __syncthreads();   // E: every read of T / Cr of this element is done
         SW_STAMP(tit, 7);
-        if (ln >= 0 && helper) {
+        if (!GT && ln >= 0 && helper) {
           if (G.npan == 1) expect_all();
           fence_proxy_async();
           load_rows(ln, (G.npan - 1) * NB, ne);
@@ -946,11 +978,11 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
   }
 }
 
-template <int NWARPS, int MAXT, int MINB>
+template <int NWARPS, int MAXT, int MINB, bool GT>
 cudaError_t launch_sweep_t(const CondenseArgs& a, int sms, cudaStream_t s) {
   const SweepGeo G(a.ne, a.nf);
-  const int64_t smem = G.smem_bytes();
-  auto kern = sweep_kernel<NWARPS, MAXT, MINB>;
+  const int64_t smem = GT ? G.smem_bytes() - 8 * ((int64_t)G.RA * G.ldT + (int64_t)G.NF8 * G.ldC) : G.smem_bytes();
+  auto kern = sweep_kernel<NWARPS, MAXT, MINB, GT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -958,6 +990,11 @@ cudaError_t launch_sweep_t(const CondenseArgs& a, int sms, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = (int64_t)sms * (per_sm < 2 ? per_sm : 2);   // the exact-path scratch holds 2 slabs per SM
+  if (GT) {
+    // one CTA per SM, and no more slabs than keep the working set L2-resident (~80 MB of the 126 MB L2)
+    const int64_t slab = 8 * ((int64_t)G.RA * G.ldT + (int64_t)G.NF8 * G.ldC);
+    grid = std::min<int64_t>(sms, std::max<int64_t>(1, (int64_t)80 * 1024 * 1024 / slab));
+  }
   if (grid > a.count) grid = a.count;
   kern<<<(unsigned)grid, NWARPS * 32, (size_t)smem, s>>>(a);
   return cudaGetLastError();
@@ -965,11 +1002,25 @@ cudaError_t launch_sweep_t(const CondenseArgs& a, int sms, cudaStream_t s) {
 
 }  // namespace
 
-// Which sweep configuration (if any) handles (ne, nf): returns the smem bytes or -1.
+// Whether the sweep kernel with T in shared memory handles (ne, nf).
 bool sweep_supported(int ne, int nf, size_t smem_optin) {
   const SweepGeo G(ne, nf);
   if ((size_t)G.smem_bytes() > smem_optin) return false;
   return (G.ntiles + 5) / 6 <= 16;
+}
+// Whether the global-slab variant handles it (elements larger than one SM: n_e <= 256, [S | g] in <= 16 slots).
+bool sweep_gt_supported(int ne, int nf) {
+  const SweepGeo G(ne, nf);
+  return ne <= kMaxNe && (G.ntiles + 5) / 6 <= 16;
+}
+
+cudaError_t launch_condense_sweep_gt(const CondenseArgs& a, int sms, cudaStream_t s, int64_t* launches) {
+  if (a.count <= 0) return cudaSuccess;
+  ++*launches;
+  const SweepGeo G(a.ne, a.nf);
+  const int slots = (G.ntiles + 5) / 6;
+  if (slots <= 11) return launch_sweep_t<8, 11, 1, true>(a, sms, s);
+  return launch_sweep_t<8, 16, 1, true>(a, sms, s);
 }
 
 cudaError_t launch_condense_sweep(const CondenseArgs& a, int sms, size_t smem_optin, cudaStream_t s, int64_t* launches) {
@@ -982,14 +1033,14 @@ cudaError_t launch_condense_sweep(const CondenseArgs& a, int sms, size_t smem_op
   // spills up to 12 [S|g] slots (checked with -Xptxas -v), and the second element hides the first's chain latency
   const bool two = 2 * (G.smem_bytes() + 1024) <= 233472 && slots <= 12;
   if (two) {
-    if (slots <= 4) return launch_sweep_t<8, 4, 2>(a, sms, s);
-    if (slots <= 7) return launch_sweep_t<8, 7, 2>(a, sms, s);
-    return launch_sweep_t<8, 12, 2>(a, sms, s);
+    if (slots <= 4) return launch_sweep_t<8, 4, 2, false>(a, sms, s);
+    if (slots <= 7) return launch_sweep_t<8, 7, 2, false>(a, sms, s);
+    return launch_sweep_t<8, 12, 2, false>(a, sms, s);
   }
-  if (slots <= 4) return launch_sweep_t<8, 4, 1>(a, sms, s);
-  if (slots <= 7) return launch_sweep_t<8, 7, 1>(a, sms, s);
-  if (slots <= 11) return launch_sweep_t<8, 11, 1>(a, sms, s);
-  return launch_sweep_t<8, 16, 1>(a, sms, s);
+  if (slots <= 4) return launch_sweep_t<8, 4, 1, false>(a, sms, s);
+  if (slots <= 7) return launch_sweep_t<8, 7, 1, false>(a, sms, s);
+  if (slots <= 11) return launch_sweep_t<8, 11, 1, false>(a, sms, s);
+  return launch_sweep_t<8, 16, 1, false>(a, sms, s);
 }
 
 }  // namespace hdg

@@ -106,6 +106,7 @@ struct Bucket {
   bool t_in_smem;     // panel kernel: working matrix in shared memory (else global scratch)
   bool sweep;         // condensed by the sweep kernel (condense_sweep.cu)
   bool warp;          // condensed by the warp-per-element kernel (condense_warp.cu)
+  bool sweep_gt;      // condensed by the sweep kernel with its working matrix in global scratch
 };
 
 // Skeleton assembly data (owned rows).
@@ -160,6 +161,8 @@ namespace hdg {
 cudaError_t launch_condense(const CondenseArgs& a, bool t_in_smem, int sms, cudaStream_t s, int64_t* launches);
 bool sweep_supported(int ne, int nf, size_t smem_optin);
 bool warp_supported(int ne, int nf);
+bool sweep_gt_supported(int ne, int nf);
+cudaError_t launch_condense_sweep_gt(const CondenseArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_condense_warp(const CondenseArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_condense_sweep(const CondenseArgs& a, int sms, size_t smem_optin, cudaStream_t s, int64_t* launches);
 cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_t* launches);
