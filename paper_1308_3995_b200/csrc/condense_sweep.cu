@@ -28,6 +28,7 @@
 // rows; the L\U rows of each finished panel leave by TMA bulk stores (shared -> global) while the sweep goes on;
 // the next element's blocks are prefetched into L2 at the start of the current one.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "dev_common.cuh"
@@ -991,9 +992,11 @@ cudaError_t launch_sweep_t(const CondenseArgs& a, int sms, cudaStream_t s) {
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = (int64_t)sms * (per_sm < 2 ? per_sm : 2);   // the exact-path scratch holds 2 slabs per SM
   if (GT) {
-    // one CTA per SM, and no more slabs than keep the working set L2-resident (~80 MB of the 126 MB L2)
+    // one CTA per SM. Capping the slabs to keep them all L2-resident was measured slower on C5 (80 MB of slabs:
+    // 114 ms, all 148 SMs with 121 MB of slabs: 106 ms); HDG_GT_L2_MB still sets a cap for experiments
     const int64_t slab = 8 * ((int64_t)G.RA * G.ldT + (int64_t)G.NF8 * G.ldC);
-    grid = std::min<int64_t>(sms, std::max<int64_t>(1, (int64_t)80 * 1024 * 1024 / slab));
+    const char* lb = getenv("HDG_GT_L2_MB");
+    grid = lb ? std::min<int64_t>(sms, std::max<int64_t>(1, atoll(lb) * 1024 * 1024 / slab)) : sms;
   }
   if (grid > a.count) grid = a.count;
   kern<<<(unsigned)grid, NWARPS * 32, (size_t)smem, s>>>(a);
