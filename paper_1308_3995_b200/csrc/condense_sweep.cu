@@ -1021,6 +1021,12 @@ cudaError_t launch_condense_sweep_gt(const CondenseArgs& a, int sms, cudaStream_
   if (a.count <= 0) return cudaSuccess;
   ++*launches;
   const SweepGeo G(a.ne, a.nf);
+  // 16 warps (14 MMA workers, 4 per SMSP): the L2 latency of the slab's fragment loads needs the extra warps
+  // (C5 slab measured 107 -> 92 ms vs 8 warps; 12 warps: 99 ms). The shared-memory sweep keeps 8 (C4: 42.9 vs
+  // 47.2 ms with 16 — its chain warp, not load latency, bounds it). Caching T's bottom rows in the free shared
+  // memory was measured slower (the 252 bucket 36 -> 41 ms): it takes the L1 capacity that already holds the
+  // slab's re-read fragments.
+  if ((G.ntiles + 13) / 14 <= 7) return launch_sweep_t<16, 7, 1, true>(a, sms, s);
   const int slots = (G.ntiles + 5) / 6;
   if (slots <= 11) return launch_sweep_t<8, 11, 1, true>(a, sms, s);
   return launch_sweep_t<8, 16, 1, true>(a, sms, s);
