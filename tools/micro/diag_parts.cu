@@ -9,6 +9,7 @@ __global__ void bench(double* LUg, long long* cyc) {
   double* T = sm;
   double* Lb = T + 120 * ldT;
   double* Ub = Lb + 2 * 16 * LDI;
+  double* St = Ub + 2 * 16 * LDI;
   const int lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 120 * ldT; i += blockDim.x) {
     const int r = i / ldT, c = i % ldT;
@@ -24,7 +25,7 @@ __global__ void bench(double* LUg, long long* cyc) {
     double* LU = LUg;
     __syncwarp();
     long long c0 = clock64();
-    viol |= lu8(T, ldT, jb, 8, Linv, Uinv, LU, ne, lane);
+    viol |= lu8(T, ldT, jb, 8, Linv, Uinv, LU, ne, St, lane);
     long long c1 = clock64();
     const int gid = lane >> 2, tig = lane & 3, c = 2 * tig;
     double* D12 = T + (size_t)jb * ldT + jb + 8;
@@ -49,7 +50,7 @@ __global__ void bench(double* LUg, long long* cyc) {
     *reinterpret_cast<double2*>(D22 + gid * ldT + c) = make_double2(d22[0], d22[1]);
     __syncwarp();
     long long c3 = clock64();
-    viol |= lu8(T, ldT, jb + 8, 8, Linv + 8 * LDI + 8, Uinv + 8 * LDI + 8, LU, ne, lane);
+    viol |= lu8(T, ldT, jb + 8, 8, Linv + 8 * LDI + 8, Uinv + 8 * LDI + 8, LU, ne, St, lane);
     long long c4 = clock64();
     double P[2] = {0.0, 0.0}, Q[2] = {0.0, 0.0};
     mm8(P, D21, ldT, Linv, LDI, 1.0, lane);

@@ -4,7 +4,7 @@
 #include <cstdio>
 namespace hdg { namespace {
 __global__ void bench(double* LUg, long long* cyc) {
-  __shared__ __align__(16) double T[16 * 20], T0[16 * 20], Li[16 * LDI], Ui[16 * LDI];
+  __shared__ __align__(16) double T[16 * 20], T0[16 * 20], Li[16 * LDI], Ui[16 * LDI], St[64];
   const int lane = threadIdx.x;
   for (int i = lane; i < 320; i += 32) T0[i] = ((i % 20) == (i / 20)) ? 4.0 + 0.1 * (i / 20) : 0.01 * ((i * 7) % 11) - 0.05;
   __syncwarp();
@@ -14,7 +14,7 @@ __global__ void bench(double* LUg, long long* cyc) {
     for (int i = lane; i < 320; i += 32) T[i] = T0[i];
     __syncwarp();
     long long t0 = clock64();
-    v |= lu8(T, 20, 0, 8, Li, Ui, LUg, 16, lane);
+    v |= lu8(T, 20, 0, 8, Li, Ui, LUg, 16, St, lane);
     long long dt = clock64() - t0;
     best = dt < best ? dt : best;
     if (r == 0) first = dt;
