@@ -10,4 +10,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 1 -c 1 -o gpurun_out/sweep_full_C4 -f python tools/prof_case.py --config C4 --reps 2 > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:condense_kernel -s 1 -c 1 -o gpurun_out/panel_full_C3 -f python tools/prof_case.py --config C3 --reps 2 > gpurun_out/ncu_full_c3.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:backsub_kernel -s 1 -c 1 -o gpurun_out/backsub_full_C4 -f python tools/prof_case.py --config C4 --reps 2 > gpurun_out/ncu_full_bs.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"sweep_kernel|condense_kernel|backsub|assemble" -c 120 --csv --log-file gpurun_out/launches_C5.csv python bench.py --config C5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_C5.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -c 1 -o gpurun_out/sweep_gt_C5 -f python bench.py --config C5 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_c5.log 2>&1
 true
