@@ -276,9 +276,9 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     // (C3: 34 vs 40 ms)
     const char* forced = getenv("HDG_CONDENSE_KERNEL");
     const std::string fk = forced ? forced : "";
-    // the warp-per-element kernel is correct (parity-tested) but measured slower than the sweep kernel on C2
-    // (1.03 vs 0.82 ms): opt-in only
-    B.warp = warp_supported(B.ne, B.nf) && fk == "warp";
+    // small elements (C1, C2): one warp per element, 16+ elements in flight per SM (C2: 0.71 ms on the sweep
+    // kernel, see DESIGN §11 for the warp kernel's number); HDG_CONDENSE_KERNEL=sweep|panel force the others
+    B.warp = warp_supported(B.ne, B.nf) && fk != "sweep" && fk != "panel";
     B.sweep = !B.warp && sweep_supported(B.ne, B.nf, ctx->smem_optin) && fk != "panel" &&
               (B.ne >= 96 || B.ne <= 32 || fk == "sweep");
     // elements larger than one SM (C5's n_e = 180, 252): the sweep kernel on an L2-resident global slab

@@ -47,27 +47,7 @@ constexpr int NB = kSweepNB;   // panel width (see diag_block for NB = 8 / 16)
   } while (0)
 constexpr int LDI = 20;   // row stride of the 16x16 inverse buffers
 
-// ------------------------------------------------------------------------------------------------------------
-// (shared helpers of the diagonal-block factorization)
-// One warp, one instruction stream (lane roles are folded into per-step coefficients, no divergence).
-// Lanes 0..15 hold row r of [block | I] and apply the elimination's row operations to both halves (the right half
-// ends as row r of L11^-1); lanes 16..31 build row i of U11^-1 by the forward recurrence z_i = 1,
-// z_c = -sum_{k<c} z_k u_kc / u_kk, U^-1[i][c] = z_c / u_cc. Step c: the pivot row c of U and row c of L11^-1 are
-// broadcast from lane c by shuffles (measured on the box: shuffles beat a shared-memory broadcast slot here,
-// 3.0K vs 4.7K cycles per block) and every lane forms 1/u_cc itself. The L\U rows are also stored to the factor
-// record LU (row-major, row stride ne) straight from registers. A partial block (nb < 16) is padded with identity
-// rows/columns. Returns true if GEPP would have interchanged rows inside the block (|a_rc| > |a_cc|, r > c) or a
-// pivot is zero, subnormal or not finite.
-constexpr int BCW = 36;   // doubles per broadcast slot: u[16] | e[16] | pad
-
-__device__ __forceinline__ void sts_if(bool p, double* addr, double v) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.f64 [%1], %2;\n}\n" ::"r"((int)p),
-               "r"(smem_u32(addr)), "d"(v));
-}
-
-__device__ __forceinline__ bool pivot_bad(double x) {
-  return !(fabs(x) >= 2.2250738585072014e-308) || !(fabs(x) < 1.0e300);
-}
+constexpr int BCW = 36;   // doubles per spare chain-warp slot (two slots: the 8x8 LU's staging copy)
 
 // ------------------------------------------------------------------------------------------------------------
 // lu8: GEPP-checked natural-order LU of the 8x8 block at (r0, r0) of X (valid size nbv <= 8, identity padding),

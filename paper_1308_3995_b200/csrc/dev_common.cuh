@@ -16,6 +16,11 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// The speculative path's pivot test (DESIGN R16): the pivot is zero, subnormal, huge or not finite.
+__device__ __forceinline__ bool pivot_bad(double x) {
+  return !(fabs(x) >= 2.2250738585072014e-308) || !(fabs(x) < 1.0e300);
+}
+
 // 1/x from MUFU.RCP64H (rcp.approx.ftz.f64, relative error ~2^-22) refined with the series
 // r (1 + e + e^2), e = 1 - x r: three dependent FMAs, result within ~1 ulp. Callers guarantee x is a normal
 // finite number (zero / subnormal / non-finite pivots are caught before and handled on the exact path).
