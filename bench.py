@@ -386,19 +386,24 @@ def main():
         cond_tflops = work["condense_flops"] / (cond_ms * 1e-3) / 1e12
         cond_gbs = work["condense_bytes"] / (cond_ms * 1e-3) / 1e9
         fp64_peak = dmma_peak or 37.2
+        # the kernel hdg_plan picks for the workload's degree buckets (api.cu dispatch)
+        kname = {"C1": "warp_kernel (condense_warp.cu)", "C2": "warp_kernel (condense_warp.cu)",
+                 "C3": "condense_kernel, panel (condense.cu)", "C4": "sweep_kernel (condense_sweep.cu)",
+                 "C5": "sweep_kernel GT/shared + condense_kernel per hp bucket (hdg_condense)"}.get(
+                     args.config, "hdg_condense")
         t_fp = work["condense_flops"] / (fp64_peak * 1e12)
         t_hbm = work["condense_bytes"] / ((hbm or 6551.4) * 1e9)
         if t_fp >= t_hbm:
             roof = {"bound": "tensor", "achieved": cond_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
                     "frac": cond_tflops / fp64_peak, "traffic": None,
-                    "kernel": "condense_kernel (hdg_condense)", "dtype": "f64 (DMMA m8n8k4 + DFMA)",
+                    "kernel": kname, "dtype": "f64 (DMMA m8n8k4 + DFMA)",
                     "peak_source": ("FP64 DMMA peak measured in this run by tools/peaks (K9)" if dmma_peak else
                                     "nominal 148 SM x 64 FP64 FMA/clk x 1.965 GHz (no in-run measurement)"),
                     "flops_per_launch": work["condense_flops"],
                     "hbm_achieved_gbs": cond_gbs, "hbm_frac": cond_gbs / (hbm or 6551.4)}
         else:
             roof = {"bound": "hbm", "achieved": cond_gbs, "peak": hbm or 6551.4, "unit": "GB/s",
-                    "frac": cond_gbs / (hbm or 6551.4), "traffic": None, "kernel": "condense_kernel (hdg_condense)",
+                    "frac": cond_gbs / (hbm or 6551.4), "traffic": None, "kernel": kname,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6551.4",
                     "bytes_per_launch": work["condense_bytes"], "fp64_tflops": cond_tflops}
         try:

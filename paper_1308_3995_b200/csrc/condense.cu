@@ -250,7 +250,9 @@ __device__ __forceinline__ void diag_inverses(const double* T, int ldT, int jb, 
   }
 }
 
-// T[jb..jb+16, c0..c0+8) <- Inv (16x16) * T[jb..jb+16, c0..c0+8), in place; one warp, one column tile.
+// T[jb..jb+16, c0..c0+8) <- Inv (16x16) * T[jb..jb+16, c0..c0+8), in place; one warp, one column tile. Inv is
+// triangular (LOWER: L^-1, else U^-1): the MMAs with its exact-zero 8x8 quadrant are skipped.
+template <bool LOWER>
 __device__ __forceinline__ void inv_times_tile(double* T, int ldT, int jb, const double* Inv, int c0, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
   double b[4];
@@ -259,8 +261,8 @@ __device__ __forceinline__ void inv_times_tile(double* T, int ldT, int jb, const
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
-    dmma(acc[0], Inv[gid * LDI + 4 * kk + tig], b[kk]);
-    dmma(acc[1], Inv[(8 + gid) * LDI + 4 * kk + tig], b[kk]);
+    if (!LOWER || kk < 2) dmma(acc[0], Inv[gid * LDI + 4 * kk + tig], b[kk]);
+    if (LOWER || kk >= 2) dmma(acc[1], Inv[(8 + gid) * LDI + 4 * kk + tig], b[kk]);
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -272,7 +274,7 @@ __device__ __forceinline__ void backsolve_tile(double* T, int ldT, int ne, const
   const int npan = (ne + NB - 1) / NB;
   for (int p = npan - 1; p >= 0; --p) {
     const int jb = p * NB;
-    inv_times_tile(T, ldT, jb, Uinv_all + p * NB * LDI, c0, lane);
+    inv_times_tile<false>(T, ldT, jb, Uinv_all + p * NB * LDI, c0, lane);
     __syncwarp();
     if (jb == 0) break;
     const int nk4 = (min(NB, ne - jb) + 3) >> 2;
@@ -312,7 +314,7 @@ __device__ __forceinline__ bool tile_times_uinv(double* T, int ldT, int jb, cons
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
-    dmma(acc[0], a[kk], Uinv[(4 * kk + tig) * LDI + gid]);
+    if (kk < 2) dmma(acc[0], a[kk], Uinv[(4 * kk + tig) * LDI + gid]);   // U^-1 upper triangular
     dmma(acc[1], a[kk], Uinv[(4 * kk + tig) * LDI + 8 + gid]);
   }
   bool viol = false;
@@ -440,7 +442,7 @@ __device__ __forceinline__ bool phase_a(double* T, const Geo& geo, double* Uinv_
     const int ri0 = (jb + NB) >> 3, nri = PIVOT ? 0 : (R >> 3) - ri0;
     bool viol = false;
     for (int job = warp; job < ncj + nri; job += NWARPS) {
-      if (job < ncj) inv_times_tile(T, ldT, jb, Linv, (cj0 + job) * 8, lane);
+      if (job < ncj) inv_times_tile<true>(T, ldT, jb, Linv, (cj0 + job) * 8, lane);
       else viol |= tile_times_uinv(T, ldT, jb, Uinv, (ri0 + job - ncj) * 8, lane);
     }
     if (!PIVOT && __any_sync(0xffffffffu, viol) && lane == 0) *spec = 1;

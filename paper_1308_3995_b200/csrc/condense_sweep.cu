@@ -300,7 +300,8 @@ __device__ __forceinline__ bool trsm_right(double* X, int ld, int r0, int nrt, i
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         if (i < nrt) {
-          dmma(acc[i][0], a[i][kk], u0);
+          // U^-1 is upper triangular: output columns 0-7 take only k < 8 (the skipped terms are exact zeros)
+          if (kk < 2) dmma(acc[i][0], a[i][kk], u0);
           if (nct > 1) dmma(acc[i][1], a[i][kk], u1);
         }
       }
@@ -346,7 +347,8 @@ __device__ __forceinline__ void trsm_left(double* T, int ld, int jb, int nb, con
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         if (j < nct) {
-          dmma(acc[0][j], l0, b[kk][j]);
+          // L^-1 is lower triangular: output rows 0-7 take only k < 8 (the skipped terms are exact zeros)
+          if (kk < 2) dmma(acc[0][j], l0, b[kk][j]);
           if (nrt > 1) dmma(acc[1][j], l1, b[kk][j]);
         }
       }
