@@ -858,7 +858,9 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
             __syncwarp();
             named_arrive(2, 96);
           }
-          for (int job = ((a.debug & 1) || helper) ? 1 << 30 : w; job < nA + nCt + nU; job += NWK) {
+          // regular jobs start from worker 2: workers 0 and 1 (which also carry the look-ahead tiles) get the
+          // remainder jobs last
+          for (int job = ((a.debug & 1) || helper) ? 1 << 30 : (w + NWK - 2) % NWK; job < nA + nCt + nU; job += NWK) {
             if (job < nA) {
               viol |= trsm_right(T, ldT, rA0 + 16 * job, min(2, tA - 2 * job), jb, nb, Uinv, ne, LU, lane);
             } else if (job < nA + nCt) {
