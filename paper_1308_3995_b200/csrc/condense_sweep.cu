@@ -759,7 +759,6 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         SW_STAMP(tit, 6);
         __syncthreads();   // E: every read of T / Cr of this element is done
         SW_STAMP(tit, 7);
-        __syncthreads();   // F: the next element's C rows are issued
       }
       SW_STAMP(tit, 101);
     }
@@ -960,7 +959,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           load_rows(ln, (G.npan - 1) * NB, ne);
           load_C(ln);
         }
-        __syncthreads();   // F
+        // no barrier here: the workers wait for these rows on the mbarrier's transaction count, the chain warp at
+        // the next element's first panel barrier (a CTA barrier here measured 0.4 ms slower on C4)
       }
       SW_STAMP(tit, 101);
     }
