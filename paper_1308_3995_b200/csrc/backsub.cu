@@ -28,7 +28,7 @@ __device__ __forceinline__ double gemv8(const double* M, int ld, int r0, int nro
   const double* Mr = M + (int64_t)(rv ? r0 + gid : 0) * ld + tig;
   double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
   int k = k0;
-#pragma unroll 2
+#pragma unroll 4
   for (; k + 8 <= k1; k += 8) {
     const double a0 = rv ? __ldg(Mr + k) : 0.0;
     const double a1 = rv ? __ldg(Mr + k + 4) : 0.0;
@@ -44,6 +44,17 @@ __device__ __forceinline__ double gemv8(const double* M, int ld, int r0, int nro
   }
   // column 0 of the tile sits in lanes with tig == 0 (element 0 of their pair); move row i's value to lane i
   return __shfl_sync(0xffffffffu, acc0[0] + acc1[0], 4 * (lane & 7));
+}
+
+// L2 prefetch of rows [r0, r0 + 8) x columns [c0, c1) of the row-major M (one 128-byte line per lane and step):
+// the next tile's matrix rows do not depend on the solve, so their HBM latency overlaps the current tile's
+__device__ __forceinline__ void prefetch_tile(const double* M, int ld, int r0, int nrows, int c0, int c1, int lane) {
+  if (c1 <= c0) return;
+  const int lines = (c1 - c0 + 15) >> 4;   // 16 doubles per 128-byte line
+  for (int q = lane; q < 8 * lines; q += 32) {
+    const int r = r0 + q / lines, c = c0 + 16 * (q % lines);
+    if (r < nrows) asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (int64_t)r * ld + c));
+  }
 }
 
 __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs a) {
@@ -95,6 +106,7 @@ __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs 
     // forward: L y = P t (unit lower)
     for (int T = 0; T < nt; ++T) {
       const int r0 = 8 * T;
+      if (T + 1 < nt) prefetch_tile(LU, ne, r0 + 8, ne, 0, r0 + 16, lane);
       const double s = T > 0 ? gemv8(LU, ne, r0, ne, 0, r0, y, lane) : 0.0;
       const int i = lane & 7, r = r0 + i;
       double Lr[8];
@@ -112,6 +124,7 @@ __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs 
     // backward: U x = y
     for (int T = nt - 1; T >= 0; --T) {
       const int r0 = 8 * T, rend = min(r0 + 8, ne);
+      if (T > 0) prefetch_tile(LU, ne, r0 - 8, ne, r0 - 8, ne, lane);
       const double s = rend < ne ? gemv8(LU, ne, r0, ne, rend, ne, y, lane) : 0.0;
       const int i = lane & 7, r = r0 + i;
       double Ur[8];
