@@ -87,7 +87,7 @@ def main():
     if a.launches:
         tot, cnt = launches(a.launches)
         path = os.path.join(PROF, f"{a.tag}_launches_{a.launch_config}.md")
-        hot = [k for k in tot if any(s in k for s in ("condense_kernel", "sweep_kernel", "assemble", "backsub", "pack",
+        hot = [k for k in tot if any(s in k for s in ("condense_kernel", "sweep_kernel", "warp_kernel", "assemble", "backsub", "pack",
                                                        "accumulate"))]
         step = sum(tot[k] / max(1, cnt[k]) for k in hot)
         with open(path, "w") as f:
