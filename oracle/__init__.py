@@ -15,6 +15,17 @@ Functions and the passages they follow (PAPER.md = /root/reference/PAPER.md, SUR
 * :func:`backsub`    O6     u_e = A_e^-1 (r_e - B_e lambda_e)   (Eq. ls)
 * :func:`monolithic` O7     dense solve of the uncondensed Eq. 44
 
+Adjoint (transposed) path — SURVEY.md §8(f) NEXT #1, PAPER.md:414-436 (§4.1 "Hybridization"):
+
+* :func:`adjoint_condense_rhs`  g~_e = r~_f - B_e^T A_e^-T r~_e   (the element part of E~ =
+  -[R^T S^T][[A B][C D]]^-T [F~; G~]; H~ = 0 gives r~_f = 0)
+* :func:`adjoint_assemble`      K~ = sum_e S_e^T and E~ = sum_e g~_e ("the hybridized adjoint system matrix is also the
+  transpose of the hybridized primal system matrix"; K^T Lambda~ = E~)
+* :func:`adjoint_backsub`       u~_e = A_e^-T (r~_e - C_e^T lambda~_e)   (the adjoint local system)
+
+Each solves with A_e^T by its own O1/O2 factorization of A_e^T (not the primal factors); pinned by
+tests/test_oracle_adjoint.py (monolithic transposed dense solve, the transpose identity, A = I closed form).
+
 Parity status: every function is pinned by tests/test_oracle.py (brute-force monolithic solve, A = I closed
 form, symmetry, LAPACK, local residuals, probe identity, pivot forcing, counts, locality, scaling).
 """
@@ -231,3 +242,67 @@ def pipeline(w, blk=None, lam=None):
     u, offU = backsub(w.elem_face, w.face_ndof, w.face_off, w.elem_ne, w.elem_nf, c["LU"], c["off_LU"], c["piv"],
                       c["off_piv"], blk["B"], blk["off_B"], blk["re"], blk["off_re"], lam)
     return dict(blk=blk, cond=c, sym=sym, K=K, E=E, lam=lam, u=u, off_u=offU)
+
+
+# ------------------------------------------------------------------------------------------------------------
+# Adjoint (transposed) path: PAPER.md:414-436. Plain per-element loops; A_e^-T by O1/O2 on A_e^T.
+def _blk(blk, key, l, shape):
+    o = int(blk["off_" + key][l])
+    return np.asarray(blk[key][o:o + shape[0] * shape[1]], dtype=np.float64).reshape(shape)
+
+
+def _gather(elem_face, face_ndof, face_off, e, vec):
+    """lambda_e: the element's faces in slot order, each face's dofs in face_off order (as O6)."""
+    out = []
+    for f in elem_face[e]:
+        if f >= 0:
+            out.append(np.asarray(vec[int(face_off[f]):int(face_off[f]) + int(face_ndof[f])], dtype=np.float64))
+    return np.concatenate(out) if out else np.zeros(0)
+
+
+def adjoint_condense_rhs(ne, nf, blk, rt_e, off_rt_e, rt_f=None, off_rt_f=None):
+    """g~_e = r~_f - B_e^T A_e^-T r~_e per element (r~_f = 0 when not given: H~ = 0).
+    Returns (g~ packed, offsets)."""
+    n = len(ne)
+    offG = _offsets(np.asarray(nf, dtype=np.int64))
+    g = np.empty(int(offG[-1]), dtype=np.float64)
+    for l in range(n):
+        a, b = int(ne[l]), int(nf[l])
+        A = _blk(blk, "A", l, (a, a))
+        B = _blk(blk, "B", l, (a, b))
+        r = np.asarray(rt_e[int(off_rt_e[l]):int(off_rt_e[l]) + a], dtype=np.float64)
+        LUt, pivt, info = lu(A.T)
+        assert info == 0, (l, info)
+        z = lu_solve(LUt, pivt, r)                       # A_e^-T r~_e
+        rf = (np.zeros(b) if rt_f is None else
+              np.asarray(rt_f[int(off_rt_f[l]):int(off_rt_f[l]) + b], dtype=np.float64))
+        g[int(offG[l]):int(offG[l]) + b] = rf - B.T @ z
+    return g, offG
+
+
+def adjoint_assemble(elem_face, face_ndof, face_off, nf, S, offS, gt, offG, sym):
+    """K~ = sum_e S_e^T, E~ = sum_e g~_e: O4 applied to the transposed element matrices."""
+    St = np.empty_like(np.asarray(S, dtype=np.float64))
+    for l in range(len(nf)):
+        b = int(nf[l])
+        o = int(offS[l])
+        St[o:o + b * b] = np.asarray(S[o:o + b * b], dtype=np.float64).reshape(b, b).T.reshape(-1)
+    return assemble(elem_face, face_ndof, face_off, nf, St, offS, gt, offG, sym)
+
+
+def adjoint_backsub(elem_face, face_ndof, face_off, ne, nf, blk, rt_e, off_rt_e, lam_t, e0: int = 0):
+    """u~_e = A_e^-T (r~_e - C_e^T lambda~_e) for elements [e0, e0 + len(ne)). Returns (u~, offsets)."""
+    n = len(ne)
+    offU = _offsets(np.asarray(ne, dtype=np.int64))
+    u = np.empty(int(offU[-1]), dtype=np.float64)
+    for l in range(n):
+        a, b = int(ne[l]), int(nf[l])
+        A = _blk(blk, "A", l, (a, a))
+        C = _blk(blk, "C", l, (b, a))
+        lam = _gather(elem_face, face_ndof, face_off, e0 + l, lam_t)
+        r = np.asarray(rt_e[int(off_rt_e[l]):int(off_rt_e[l]) + a], dtype=np.float64)
+        LUt, pivt, info = lu(A.T)
+        assert info == 0, (l, info)
+        u[int(offU[l]):int(offU[l]) + a] = lu_solve(LUt, pivt, r - C.T @ lam)
+    return u, offU
+
