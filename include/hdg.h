@@ -157,6 +157,29 @@ hdg_status hdg_skeleton_accumulate(hdg_ctx ctx, const double* recv, double* K, d
 hdg_status hdg_backsubstitute(hdg_ctx ctx, const void* factors, const double* B, const double* r_e,
                               const double* lambda, double* u, hdg_stream stream);
 
+/* ---- adjoint (transposed) use of the same factors: SURVEY.md §8(f) NEXT #1, PAPER.md:414-436 ----------------
+ * The adjoint local matrix is the transpose of the primal one and the hybridized adjoint matrix
+ * is K^T, so the adjoint reuses the plan and the factors of hdg_condense (same element degrees). */
+
+/* Adjoint right-hand side, element part of E~ = -[R^T S^T][[A B][C D]]^-T [F~; G~]:
+ * g~_e = r~_f - B_e^T A_e^-T r~_e for every local element. factors, B: as for hdg_backsubstitute. rt_e: packed
+ * like r_e; rt_f: packed like r_f, or NULL for r~_f = 0 (H~ = 0). gt: packed like g (output).
+ * All device pointers, 16-byte aligned. */
+hdg_status hdg_condense_adjoint_rhs(hdg_ctx ctx, const void* factors, const double* B, const double* rt_e,
+                                    const double* rt_f, double* gt, hdg_stream stream);
+
+/* Adjoint skeleton assembly: Kt = sum_e S_e^T (= K^T block by block) into the plan's block-CSR
+ * structure (same row_ptr / col_idx / blk_off as hdg_assemble_skeleton), Et = sum_e g~_e, left then right.
+ * S from hdg_condense, gt from hdg_condense_adjoint_rhs. One rank only in this version (HDG_ERR_UNSUPPORTED when
+ * the plan has shared-face exchange items). */
+hdg_status hdg_assemble_adjoint(hdg_ctx ctx, const double* S, const double* gt, double* Kt, double* Et,
+                                hdg_stream stream);
+
+/* Adjoint reconstruction: u~_e = A_e^-T (r~_e - C_e^T lambda~_e), lambda~_e gathered from the
+ * adjoint trace vector lambda_t [n_trace] in slot order. C: the packed input of hdg_condense. ut: packed like u. */
+hdg_status hdg_backsubstitute_adjoint(hdg_ctx ctx, const void* factors, const double* C, const double* rt_e,
+                                      const double* lambda_t, double* ut, hdg_stream stream);
+
 /* Lowest local element with info != 0 (synchronizes stream). Returns HDG_OK with *elem = -1 if none, or
  * HDG_ERR_SINGULAR with the element (local index) and its info code ("singular local block -> diagnostic
  * naming the element"). */

@@ -78,6 +78,12 @@ def lib():
         L.hdg_skeleton_accumulate.argtypes = [P, P, P, P, P]
         L.hdg_backsubstitute.restype = I32
         L.hdg_backsubstitute.argtypes = [P] + [P] * 5 + [P]
+        L.hdg_condense_adjoint_rhs.restype = I32
+        L.hdg_condense_adjoint_rhs.argtypes = [P] + [P] * 5 + [P]
+        L.hdg_assemble_adjoint.restype = I32
+        L.hdg_assemble_adjoint.argtypes = [P] + [P] * 4 + [P]
+        L.hdg_backsubstitute_adjoint.restype = I32
+        L.hdg_backsubstitute_adjoint.argtypes = [P] + [P] * 5 + [P]
         L.hdg_first_error.restype = I32
         L.hdg_first_error.argtypes = [P, P, ctypes.POINTER(I64), ctypes.POINTER(ctypes.c_int32), P]
         L.hdg_launch_count.restype = I64
@@ -95,7 +101,8 @@ def lib():
 EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status_string", "hdg_ctx_create",
             "hdg_ctx_destroy", "hdg_last_error", "hdg_plan", "hdg_condense", "hdg_assemble_skeleton",
             "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
-            "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout")
+            "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout", "hdg_condense_adjoint_rhs",
+            "hdg_assemble_adjoint", "hdg_backsubstitute_adjoint")
 
 
 def _ptr(t):
@@ -250,6 +257,25 @@ class Context:
         _f64(B, r_e, lam, u)
         self._check(self._L.hdg_backsubstitute(self._h, *map(_ptr, (factors, B, r_e, lam, u)), _stream(stream)),
                     "hdg_backsubstitute")
+
+    # ---- adjoint (transposed) path: SURVEY.md §8(f) NEXT #1, PAPER.md:414-436 ---------------------------------------
+    def condense_adjoint_rhs(self, factors, B, rt_e, rt_f, gt, stream=None):
+        """g~_e = r~_f - B_e^T A_e^-T r~_e (rt_f None: r~_f = 0, H~ = 0)."""
+        _f64(B, rt_e, gt)
+        self._check(self._L.hdg_condense_adjoint_rhs(self._h, *map(_ptr, (factors, B, rt_e, rt_f, gt)),
+                                                     _stream(stream)), "hdg_condense_adjoint_rhs")
+
+    def assemble_adjoint(self, S, gt, Kt, Et, stream=None):
+        """Kt = sum_e S_e^T (= K^T), Et = sum_e g~_e."""
+        _f64(S, gt, Kt, Et)
+        self._check(self._L.hdg_assemble_adjoint(self._h, *map(_ptr, (S, gt, Kt, Et)), _stream(stream)),
+                    "hdg_assemble_adjoint")
+
+    def backsubstitute_adjoint(self, factors, C, rt_e, lam_t, ut, stream=None):
+        """u~_e = A_e^-T (r~_e - C_e^T lambda~_e)."""
+        _f64(C, rt_e, lam_t, ut)
+        self._check(self._L.hdg_backsubstitute_adjoint(self._h, *map(_ptr, (factors, C, rt_e, lam_t, ut)),
+                                                       _stream(stream)), "hdg_backsubstitute_adjoint")
 
     def first_error(self, info, stream=None):
         e = ctypes.c_int64()

@@ -459,6 +459,64 @@ hdg_status hdg_backsubstitute(hdg_ctx ctx, const void* factors, const double* B,
   return HDG_OK;
 }
 
+// ---- adjoint (transposed) path: SURVEY.md §8(f) NEXT #1, PAPER.md:414-436 ---------------------------------------
+static hdg_status adjoint_elementwise(hdg_ctx ctx, int mode, const char* name, const void* factors, const double* M,
+                                      const double* rt_e, const double* rt_f, const double* lambda_t, double* out,
+                                      hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "%s: no plan", name);
+  ctx->launches = 0;
+  if (p.n == 0) return HDG_OK;
+  const void* ptrs[] = {factors, M, rt_e, out};
+  for (const void* q : ptrs)
+    if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "%s: null or misaligned (16 B) pointer", name);
+  if (mode == 1 && !lambda_t && p.n_trace > 0) return fail(ctx, HDG_ERR_ARG, "%s: null lambda_t", name);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  for (const Bucket& b : p.buckets) {
+    AdjointArgs a;
+    a.factors = static_cast<const unsigned char*>(factors);
+    a.re = rt_e; a.rf = rt_f; a.M = M; a.lambda = lambda_t; a.out = out;
+    a.elems = b.d_elems;
+    a.offF = p.d_off[OFF_F]; a.offRe = p.d_off[OFF_RE]; a.offRf = p.d_off[OFF_RF];
+    a.offM = p.d_off[mode == 0 ? OFF_B : OFF_C];
+    a.offOut = p.d_off[mode == 0 ? OFF_G : OFF_U];
+    a.elem_face = p.d_elem_face; a.face_ndof = p.d_face_ndof; a.face_off = p.d_face_off;
+    a.elem_begin = p.eb;
+    a.ne = b.ne; a.nf = b.nf; a.count = b.count;
+    HDG_CUDA(ctx, launch_adjoint(a, mode, ctx->sms, s, &ctx->launches));
+  }
+  return HDG_OK;
+}
+
+hdg_status hdg_condense_adjoint_rhs(hdg_ctx ctx, const void* factors, const double* B, const double* rt_e,
+                                    const double* rt_f, double* gt, hdg_stream stream) {
+  if (rt_f && !aligned16(rt_f)) return fail(ctx, HDG_ERR_ARG, "hdg_condense_adjoint_rhs: misaligned rt_f");
+  return adjoint_elementwise(ctx, 0, "hdg_condense_adjoint_rhs", factors, B, rt_e, rt_f, nullptr, gt, stream);
+}
+
+hdg_status hdg_backsubstitute_adjoint(hdg_ctx ctx, const void* factors, const double* C, const double* rt_e,
+                                      const double* lambda_t, double* ut, hdg_stream stream) {
+  return adjoint_elementwise(ctx, 1, "hdg_backsubstitute_adjoint", factors, C, rt_e, nullptr, lambda_t, ut, stream);
+}
+
+hdg_status hdg_assemble_adjoint(hdg_ctx ctx, const double* S, const double* gt, double* Kt, double* Et,
+                                hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_assemble_adjoint: no plan");
+  ctx->launches = 0;
+  if ((p.sk.nvals > 0 && !Kt) || (p.sk.ntr > 0 && !Et) || (p.n > 0 && (!S || !gt)))
+    return fail(ctx, HDG_ERR_ARG, "hdg_assemble_adjoint: null pointer");
+  if (p.sk.n_send_items > 0 || p.sk.n_recv_items > 0)
+    return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_assemble_adjoint: shared-face exchange not supported yet");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  HDG_CUDA(ctx, launch_assemble(p, S, gt, Kt, Et, nullptr, s, &ctx->launches, true));
+  return HDG_OK;
+}
+
 hdg_status hdg_first_error(hdg_ctx ctx, const int32_t* info, int64_t* elem, int32_t* code, hdg_stream stream) {
   if (!ctx || !elem || !code) return HDG_ERR_ARG;
   const Plan& p = ctx->plan;

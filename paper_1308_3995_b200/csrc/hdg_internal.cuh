@@ -99,6 +99,20 @@ struct BacksubArgs {
   int64_t count;
 };
 
+struct AdjointArgs {
+  const unsigned char* factors;
+  const double *re, *rf, *M, *lambda;   // M = B_e (adjoint rhs) or C_e (adjoint reconstruction)
+  double* out;                          // g~ or u~
+  const int32_t* elems;
+  const int64_t *offF, *offRe, *offRf, *offM, *offOut;
+  const int32_t* elem_face;
+  const int32_t* face_ndof;
+  const int64_t* face_off;
+  int64_t elem_begin;
+  int ne, nf;
+  int64_t count;
+};
+
 struct Bucket {
   int ne, nf;
   int64_t count;
@@ -166,9 +180,10 @@ cudaError_t launch_condense_sweep_gt(const CondenseArgs& a, int sms, cudaStream_
 cudaError_t launch_condense_warp(const CondenseArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_condense_sweep(const CondenseArgs& a, int sms, size_t smem_optin, cudaStream_t s, int64_t* launches);
 cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_t* launches);
+cudaError_t launch_adjoint(const AdjointArgs& a, int mode, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s);
 cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, double* K, double* E, double* send,
-                            cudaStream_t s, int64_t* launches);
+                            cudaStream_t s, int64_t* launches, bool transposed = false);
 cudaError_t launch_accumulate(const Plan& p, const double* recv, double* K, double* E, cudaStream_t s,
                               int64_t* launches);
 cudaError_t launch_first_error(const int32_t* info, int64_t n, int64_t* d_out, cudaStream_t s);

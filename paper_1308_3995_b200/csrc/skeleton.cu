@@ -110,7 +110,9 @@ __device__ __forceinline__ int slot_of(const int32_t* elem_face, const int32_t* 
   return s;
 }
 
-// a6: one warp per K block; left contribution first, then right: K = (0 + S_left) + S_right
+// a6: one warp per K block; left contribution first, then right: K = (0 + S_left) + S_right.
+// TR (adjoint): K~ = sum_e S_e^T, i.e. block (f, f') takes S_e[slot f' rows, slot f cols]^T.
+template <bool TR>
 __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -129,15 +131,15 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs a) {
     if (slot_of(a.elem_face, a.face_ndof, e, c, &so_b) < 0) continue;
     const int64_t l = e - a.eb;
     ld[ns] = a.nf[l];
-    src[ns] = a.S + a.offS[l] + (int64_t)so_a * ld[ns] + so_b;
+    src[ns] = TR ? a.S + a.offS[l] + (int64_t)so_b * ld[ns] + so_a : a.S + a.offS[l] + (int64_t)so_a * ld[ns] + so_b;
     ++ns;
   }
   double* dst = a.K + a.blk_off[q];
   for (int idx = lane; idx < na * nb; idx += 32) {
     const int r = idx / nb, cc = idx - r * nb;
     double v = 0.0;
-    if (ns > 0) v = v + __ldg(src[0] + (int64_t)r * ld[0] + cc);
-    if (ns > 1) v = v + __ldg(src[1] + (int64_t)r * ld[1] + cc);
+    if (ns > 0) v = v + __ldg(TR ? src[0] + (int64_t)cc * ld[0] + r : src[0] + (int64_t)r * ld[0] + cc);
+    if (ns > 1) v = v + __ldg(TR ? src[1] + (int64_t)cc * ld[1] + r : src[1] + (int64_t)r * ld[1] + cc);
     dst[idx] = v;
   }
 }
@@ -268,9 +270,13 @@ cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s) {
 }
 
 cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, double* K, double* E, double* send,
-                            cudaStream_t s, int64_t* launches) {
+                            cudaStream_t s, int64_t* launches, bool transposed) {
   const AsmArgs a = make_args(p, S, g, K, E);
-  if (p.sk.nnzb > 0) { assemble_kernel<<<blocks_for(32 * p.sk.nnzb), 256, 0, s>>>(a); ++*launches; }
+  if (p.sk.nnzb > 0) {
+    if (transposed) assemble_kernel<true><<<blocks_for(32 * p.sk.nnzb), 256, 0, s>>>(a);
+    else assemble_kernel<false><<<blocks_for(32 * p.sk.nnzb), 256, 0, s>>>(a);
+    ++*launches;
+  }
   if (p.sk.f1 > p.sk.f0) { assemble_rhs_kernel<<<blocks_for(32 * (p.sk.f1 - p.sk.f0)), 256, 0, s>>>(a); ++*launches; }
   if (p.sk.n_send_items > 0) {
     pack_kernel<<<blocks_for(32 * p.sk.n_send_items), 256, 0, s>>>(a, p.sk.d_send_items, p.sk.n_send_items, send);

@@ -1,0 +1,88 @@
+"""GPU parity of the adjoint (transposed) path — SURVEY.md §8(f) NEXT #1, PAPER.md:414-436 — through the C ABI.
+
+hdg_condense_adjoint_rhs (g~_e = r~_f - B_e^T A_e^-T r~_e), hdg_assemble_adjoint (K~ = sum_e S_e^T, E~ = sum g~_e)
+and hdg_backsubstitute_adjoint (u~_e = A_e^-T (r~_e - C_e^T lambda~_e)) reuse the plan and the factors of the primal
+hdg_condense; the oracle solves with its own factorization of A_e^T (oracle.adjoint_*). Bars as for the primal:
+g~, u~ within 1e-11 relative (Frobenius, per element); the adjoint assembly of the GPU's own S bitwise equal to
+the oracle's adjoint assembly of the same S; the assembled K~ equal to K^T entry by entry (the transpose identity,
+SPEC.md:512, 720).
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from gpu_helpers import rel_fro_per_element, run_gpu, to_dev
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+def _adjoint_case(w, blk, with_rf=False, seed=17):
+    import torch
+    rng = np.random.default_rng(seed)
+    rt = rng.standard_normal(int(np.sum(w.elem_ne)))
+    rtf = rng.standard_normal(int(np.sum(w.elem_nf))) if with_rf else None
+    lam_t = rng.standard_normal(int(w.face_off[-1]))
+    r = run_gpu(w, blk=blk)
+    ctx, d = r["ctx"], r["dev"]
+    gt, ut = ctx.alloc("g"), ctx.alloc("u")
+    Kt, Et = ctx.alloc("K"), ctx.alloc("E")
+    rt_d = to_dev(rt)
+    ctx.condense_adjoint_rhs(r["factors"], d["B"], rt_d, to_dev(rtf) if with_rf else None, gt)
+    ctx.assemble_adjoint(r["S"], gt, Kt, Et)
+    ctx.backsubstitute_adjoint(r["factors"], d["C"], rt_d, to_dev(lam_t), ut)
+    torch.cuda.synchronize()
+    offG = np.concatenate([[0], np.cumsum(np.asarray(w.elem_nf, dtype=np.int64))])
+    g_ref, _ = oracle.adjoint_condense_rhs(w.elem_ne, w.elem_nf, blk, rt, blk["off_re"], rtf,
+                                           offG if with_rf else None)
+    u_ref, offU = oracle.adjoint_backsub(w.elem_face, w.face_ndof, w.face_off, w.elem_ne, w.elem_nf, blk, rt,
+                                         blk["off_re"], lam_t)
+    eg = rel_fro_per_element(gt.cpu().numpy()[:len(g_ref)], g_ref, offG)
+    eu = rel_fro_per_element(ut.cpu().numpy()[:len(u_ref)], u_ref, offU)
+    assert eg < TOL, eg
+    assert eu < TOL, eu
+    # adjoint assembly: bitwise against the oracle's adjoint assembly of the GPU's own S and g~; and = K^T
+    S_gpu = r["S"].cpu().numpy()
+    g_gpu = gt.cpu().numpy()
+    offS = np.concatenate([[0], np.cumsum(np.asarray(w.elem_nf, dtype=np.int64) ** 2)])
+    sym = oracle.symbolic(w.elem_face, w.face_elem, w.face_ndof)
+    Kt_ref, Et_ref = oracle.adjoint_assemble(w.elem_face, w.face_ndof, w.face_off, w.elem_nf, S_gpu[:offS[-1]], offS,
+                                             g_gpu[:offG[-1]], offG, sym)
+    nv = len(Kt_ref)
+    assert np.array_equal(Kt.cpu().numpy()[:nv], Kt_ref)
+    assert np.array_equal(Et.cpu().numpy()[:len(Et_ref)], Et_ref)
+    Kd = oracle.to_dense(sym, r["K"].cpu().numpy()[:nv], w.face_ndof, w.face_off)
+    Ktd = oracle.to_dense(sym, Kt.cpu().numpy()[:nv], w.face_ndof, w.face_off)
+    assert np.array_equal(Ktd, Kd.T)
+
+
+@pytest.mark.parametrize("name,nr,nt", [("C1", 16, 32), ("C2", 4, 8), ("C3", 2, 6), ("C4", 2, 4), ("C5", 2, 6)])
+def test_adjoint_parity(cuda, name, nr, nt):
+    w = gen.config(name, nr=nr, nt=nt)
+    _adjoint_case(w, gen.host_blocks(w))
+
+
+def test_adjoint_with_rf_and_paper_boundary(cuda):
+    w = gen.config("C3", nr=2, nt=5, boundary="paper")
+    _adjoint_case(w, gen.host_blocks(w), with_rf=True, seed=23)
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_adjoint_pivot_forcing(cuda, name):
+    """Row-permuted (A, B, r_e): the saved factors carry a non-trivial permutation, which the transposed solves
+    must undo (z[perm[i]] = y[i])."""
+    w = gen.config(name, nr=2, nt=4)
+    blk = gen.host_blocks(w)
+    rng = np.random.default_rng(29)
+    for e in range(w.E):
+        ne, nf = int(w.elem_ne[e]), int(w.elem_nf[e])
+        A = blk["A"][blk["off_A"][e]:blk["off_A"][e + 1]].reshape(ne, ne)
+        B = blk["B"][blk["off_B"][e]:blk["off_B"][e + 1]].reshape(ne, nf)
+        re = blk["re"][blk["off_re"][e]:blk["off_re"][e + 1]]
+        P = rng.permutation(ne)
+        A[...] = A[P]
+        B[...] = B[P]
+        re[...] = re[P]
+    _adjoint_case(w, blk, seed=31)
