@@ -44,6 +44,77 @@ def algorithmic(ne, nf):
                 backsub_bytes=float(bb.sum()))
 
 
+def run_adjoint(args, wl, rank, world, local):
+    """The adjoint (transposed) step on the primal factors — g~ = r~_f - B^T A^-T r~_e, K~ = sum S_e^T, E~ = sum g~,
+    u~ = A^-T (r~_e - C^T lambda~) — timed like the primal step. One rank (the adjoint assembly
+    has no shared-face exchange yet)."""
+    import torch
+    if world > 1:
+        raise SystemExit("--path adjoint: one rank only in this version")
+    w, ctx, stream, inp, lam = wl["w"], wl["ctx"], wl["stream"], wl["inp"], wl["lam"]
+    S, F, infot, K, E = (wl[k] for k in ("S", "F", "infot", "K", "E"))
+    eb, n = wl["eb"], wl["n"]
+    gt, ut = ctx.alloc("g"), ctx.alloc("u")
+    ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], S, wl["g"], F, infot, stream=stream)
+    rt, lam_t = inp["re"], lam      # seeded stand-ins for the functional's linearization and the adjoint trace
+    launches = [0]
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        ctx.condense_adjoint_rhs(F, inp["B"], rt, None, gt, stream=stream)
+        launches[0] += ctx.launch_count()
+        if ev:
+            ev[1].record(stream)
+        ctx.assemble_adjoint(S, gt, K, E, stream=stream)
+        launches[0] += ctx.launch_count()
+        if ev:
+            ev[2].record(stream)
+        ctx.backsubstitute_adjoint(F, inp["C"], rt, lam_t, ut, stream=stream)
+        launches[0] += ctx.launch_count()
+        if ev:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches[0] = 0
+    for i in range(args.steps):
+        step(evs[i])
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    rhs_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    asm_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    bs_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    ms_step = sum(e[0].elapsed_time(e[3]) for e in evs) / args.steps
+    ne = np.asarray(w.elem_ne[eb:eb + n], dtype=np.float64)
+    nf = np.asarray(w.elem_nf[eb:eb + n], dtype=np.float64)
+    fac = 8 * ne * ne + 4 * ne
+    rhs_bytes = float((fac + 8 * ne * nf + 8 * ne + 8 * nf).sum())        # factors, B, r~_e, g~
+    bs_bytes = float((fac + 8 * nf * ne + 16 * ne + 8 * nf).sum())        # factors, C, r~_e, lambda~_e, u~
+    hbm = measured_peaks().get("hbm_gbs") or 6551.4
+    ach = (rhs_bytes + bs_bytes) / ((rhs_ms + bs_ms) * 1e-3) / 1e9
+    line = {"metric": "adjoint element steps/s (fp64): adjoint rhs + K^T assembly + adjoint reconstruction",
+            "value": n / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "impl": "hdg", "path": "adjoint",
+            "data": "synthetic (seeded Philox blocks; r~_e, lambda~ seeded stand-ins)",
+            "config": {"workload": args.config, "elements": int(n), "n_e": int(ne.max()), "n_f": int(nf.max()),
+                       "step": "condense_adjoint_rhs + assemble_adjoint + backsubstitute_adjoint"},
+            "adjoint_rhs_ms": rhs_ms, "assemble_adjoint_ms": asm_ms, "backsub_adjoint_ms": bs_ms,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                         "traffic": None, "kernel": "adjoint_kernel<0, 1> (adjoint.cu)",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                         "bytes_per_step": rhs_bytes + bs_bytes},
+            "gpu_launches": launches[0], "clocks": clk, "e2e": None, "cpu_baseline": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def measured_peaks():
     peaks = {}
     try:
@@ -256,6 +327,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--path", default="primal", choices=["primal", "adjoint"],
+                    help="adjoint: time the transposed path (SURVEY.md §8(f) NEXT #1) on the primal factors")
     ap.add_argument("--slab", default=None,
                     help="r/P: time rank r's slab of a P-way partition on this one GPU (default for C5: 0/8)")
     args = ap.parse_args()
@@ -283,6 +356,8 @@ def main():
     dmma_peak, dfma_peak = (fp64_peak_in_run() if rank == 0 else (None, None))
 
     wl = setup_workload(args.config, rank, world, local, slab=args.slab)
+    if args.path == "adjoint":
+        return run_adjoint(args, wl, rank, world, local)
     w, ctx, info, stream, inp, lam = wl["w"], wl["ctx"], wl["info"], wl["stream"], wl["inp"], wl["lam"]
     S, g, u, F, infot, K, E, send, recv = (wl[k] for k in ("S", "g", "u", "F", "infot", "K", "E", "send", "recv"))
     eb, n, reb = wl["eb"], wl["n"], wl["reb"]

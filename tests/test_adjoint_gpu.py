@@ -86,3 +86,34 @@ def test_adjoint_pivot_forcing(cuda, name):
         B[...] = B[P]
         re[...] = re[P]
     _adjoint_case(w, blk, seed=31)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_adjoint_full_size_sampled(cuda, name):
+    """BASELINE.json full size in bench.py's launch configuration (bench.setup_workload, the adjoint step as
+    `bench.py --path adjoint` times it): sampled elements' g~ and u~ against the oracle one by one."""
+    import torch
+    import bench
+    wl = bench.setup_workload(name)
+    w, ctx, inp, n = wl["w"], wl["ctx"], wl["inp"], wl["n"]
+    ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], wl["S"], wl["g"], wl["F"], wl["infot"])
+    gt, ut = ctx.alloc("g"), ctx.alloc("u")
+    ctx.condense_adjoint_rhs(wl["F"], inp["B"], inp["re"], None, gt)
+    ctx.backsubstitute_adjoint(wl["F"], inp["C"], inp["re"], wl["lam"], ut)
+    torch.cuda.synchronize()
+    lam_t = wl["lam"].cpu().numpy()
+    rng = np.random.default_rng(20261020)
+    loc = np.unique(np.concatenate([np.arange(3), n - 1 - np.arange(3), rng.integers(0, n, 16)]))
+    ne_l, nf_l = w.elem_ne.astype(np.int64), w.elem_nf.astype(np.int64)
+    offG = np.concatenate([[0], np.cumsum(nf_l)])
+    offU = np.concatenate([[0], np.cumsum(ne_l)])
+    for e in loc:
+        e = int(e)
+        blk = gen.host_blocks(w, e, 1)
+        g_ref, _ = oracle.adjoint_condense_rhs(w.elem_ne[e:e + 1], w.elem_nf[e:e + 1], blk, blk["re"], blk["off_re"])
+        u_ref, _ = oracle.adjoint_backsub(w.elem_face, w.face_ndof, w.face_off, w.elem_ne[e:e + 1],
+                                          w.elem_nf[e:e + 1], blk, blk["re"], blk["off_re"], lam_t, e0=e)
+        g = gt[int(offG[e]):int(offG[e + 1])].cpu().numpy()
+        u = ut[int(offU[e]):int(offU[e + 1])].cpu().numpy()
+        assert np.linalg.norm(g - g_ref) / np.linalg.norm(g_ref) < TOL, (name, e)
+        assert np.linalg.norm(u - u_ref) / np.linalg.norm(u_ref) < TOL, (name, e)
