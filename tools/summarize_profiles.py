@@ -106,7 +106,8 @@ def main():
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for rep, cfg in zip(a.rep, a.config):
         m, kname = raw_metrics(rep)
-        short = ("condense_sweep" if "sweep_kernel" in kname else "condense" if "condense" in kname else
+        short = ("condense_sweep" if "sweep_kernel" in kname else "adjoint" if "adjoint" in kname else
+                 "condense" if "condense" in kname else
                  "backsub" if "backsub" in kname else "".join(ch for ch in kname.split("(")[0][-30:] if ch.isalnum()))
         path = os.path.join(PROF, f"{a.tag}_{short}_{cfg}_ncu.md")
         with open(path, "w") as f:
