@@ -66,7 +66,7 @@ def run_adjoint(args, wl, rank, world, local):
         launches[0] += ctx.launch_count()
         if ev:
             ev[1].record(stream)
-        ctx.assemble_adjoint(S, gt, K, E, stream=stream)
+        ctx.assemble_adjoint(S, gt, K, E, send=wl["send"], stream=stream)
         launches[0] += ctx.launch_count()
         if ev:
             ev[2].record(stream)

@@ -170,10 +170,11 @@ hdg_status hdg_condense_adjoint_rhs(hdg_ctx ctx, const void* factors, const doub
 
 /* Adjoint skeleton assembly: Kt = sum_e S_e^T (= K^T block by block) into the plan's block-CSR
  * structure (same row_ptr / col_idx / blk_off as hdg_assemble_skeleton), Et = sum_e g~_e, left then right.
- * S from hdg_condense, gt from hdg_condense_adjoint_rhs. One rank only in this version (HDG_ERR_UNSUPPORTED when
- * the plan has shared-face exchange items). */
+ * S from hdg_condense, gt from hdg_condense_adjoint_rhs. With nranks > 1, send (plan.send_doubles, device) receives
+ * this rank's contributions to rows owned by others (strips of S_e^T, same layout as hdg_assemble_skeleton's);
+ * after the transport, hdg_skeleton_accumulate(recv, Kt, Et) finishes the owned rows (bitwise as one rank). */
 hdg_status hdg_assemble_adjoint(hdg_ctx ctx, const double* S, const double* gt, double* Kt, double* Et,
-                                hdg_stream stream);
+                                double* send, hdg_stream stream);
 
 /* Adjoint reconstruction: u~_e = A_e^-T (r~_e - C_e^T lambda~_e), lambda~_e gathered from the
  * adjoint trace vector lambda_t [n_trace] in slot order. C: the packed input of hdg_condense. ut: packed like u. */

@@ -81,7 +81,7 @@ def lib():
         L.hdg_condense_adjoint_rhs.restype = I32
         L.hdg_condense_adjoint_rhs.argtypes = [P] + [P] * 5 + [P]
         L.hdg_assemble_adjoint.restype = I32
-        L.hdg_assemble_adjoint.argtypes = [P] + [P] * 4 + [P]
+        L.hdg_assemble_adjoint.argtypes = [P] + [P] * 5 + [P]
         L.hdg_backsubstitute_adjoint.restype = I32
         L.hdg_backsubstitute_adjoint.argtypes = [P] + [P] * 5 + [P]
         L.hdg_first_error.restype = I32
@@ -265,10 +265,10 @@ class Context:
         self._check(self._L.hdg_condense_adjoint_rhs(self._h, *map(_ptr, (factors, B, rt_e, rt_f, gt)),
                                                      _stream(stream)), "hdg_condense_adjoint_rhs")
 
-    def assemble_adjoint(self, S, gt, Kt, Et, stream=None):
-        """Kt = sum_e S_e^T (= K^T), Et = sum_e g~_e."""
-        _f64(S, gt, Kt, Et)
-        self._check(self._L.hdg_assemble_adjoint(self._h, *map(_ptr, (S, gt, Kt, Et)), _stream(stream)),
+    def assemble_adjoint(self, S, gt, Kt, Et, send=None, stream=None):
+        """Kt = sum_e S_e^T (= K^T), Et = sum_e g~_e (send: contributions to other ranks' rows)."""
+        _f64(S, gt, Kt, Et, send)
+        self._check(self._L.hdg_assemble_adjoint(self._h, *map(_ptr, (S, gt, Kt, Et, send)), _stream(stream)),
                     "hdg_assemble_adjoint")
 
     def backsubstitute_adjoint(self, factors, C, rt_e, lam_t, ut, stream=None):

@@ -502,18 +502,17 @@ hdg_status hdg_backsubstitute_adjoint(hdg_ctx ctx, const void* factors, const do
 }
 
 hdg_status hdg_assemble_adjoint(hdg_ctx ctx, const double* S, const double* gt, double* Kt, double* Et,
-                                hdg_stream stream) {
+                                double* send, hdg_stream stream) {
   if (!ctx) return HDG_ERR_ARG;
   const Plan& p = ctx->plan;
   if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_assemble_adjoint: no plan");
   ctx->launches = 0;
   if ((p.sk.nvals > 0 && !Kt) || (p.sk.ntr > 0 && !Et) || (p.n > 0 && (!S || !gt)))
     return fail(ctx, HDG_ERR_ARG, "hdg_assemble_adjoint: null pointer");
-  if (p.sk.n_send_items > 0 || p.sk.n_recv_items > 0)
-    return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_assemble_adjoint: shared-face exchange not supported yet");
+  if (p.sk.send_doubles > 0 && !send) return fail(ctx, HDG_ERR_ARG, "hdg_assemble_adjoint: send buffer required");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   HDG_CUDA(ctx, cudaSetDevice(ctx->device));
-  HDG_CUDA(ctx, launch_assemble(p, S, gt, Kt, Et, nullptr, s, &ctx->launches, true));
+  HDG_CUDA(ctx, launch_assemble(p, S, gt, Kt, Et, send, s, &ctx->launches, true));
   return HDG_OK;
 }
 

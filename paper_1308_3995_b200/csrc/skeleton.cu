@@ -170,7 +170,9 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(const AsmArgs a) {
 }
 
 // a7 pack: item (face f, local element l, offset o): send[o .. o+na) = g_l[slot f], then the na x nf_l strip
-// S_l[slot f rows, all columns] (row-major). One warp per item.
+// S_l[slot f rows, all columns] (row-major). One warp per item. TR (adjoint): the strip of S_l^T, i.e. S_l's
+// slot-f columns, so that the owner's ordered accumulate builds K~ = sum S_e^T exactly as K.
+template <bool TR>
 __global__ void __launch_bounds__(256) pack_kernel(const AsmArgs a, const int64_t* items, int64_t n_items, double* send) {
   const int lane = threadIdx.x & 31;
   const int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -182,9 +184,12 @@ __global__ void __launch_bounds__(256) pack_kernel(const AsmArgs a, const int64_
   slot_of(a.elem_face, a.face_ndof, e, f, &so);
   const int na = a.face_ndof[f], nfl = a.nf[l];
   const double* g = a.g + a.offG[l] + so;
-  const double* S = a.S + a.offS[l] + (int64_t)so * nfl;
+  const double* S = a.S + a.offS[l] + (TR ? so : (int64_t)so * nfl);
   for (int i = lane; i < na; i += 32) send[o + i] = g[i];
-  for (int i = lane; i < na * nfl; i += 32) send[o + na + i] = S[i];
+  for (int i = lane; i < na * nfl; i += 32) {
+    const int r = i / nfl, c = i - r * nfl;
+    send[o + na + i] = TR ? S[(int64_t)c * nfl + r] : S[i];
+  }
 }
 
 // a7 accumulate: item (owned face f, remote element e, offset o): add the strip into row f's blocks and E[f]
@@ -279,7 +284,8 @@ cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, dou
   }
   if (p.sk.f1 > p.sk.f0) { assemble_rhs_kernel<<<blocks_for(32 * (p.sk.f1 - p.sk.f0)), 256, 0, s>>>(a); ++*launches; }
   if (p.sk.n_send_items > 0) {
-    pack_kernel<<<blocks_for(32 * p.sk.n_send_items), 256, 0, s>>>(a, p.sk.d_send_items, p.sk.n_send_items, send);
+    if (transposed) pack_kernel<true><<<blocks_for(32 * p.sk.n_send_items), 256, 0, s>>>(a, p.sk.d_send_items, p.sk.n_send_items, send);
+    else pack_kernel<false><<<blocks_for(32 * p.sk.n_send_items), 256, 0, s>>>(a, p.sk.d_send_items, p.sk.n_send_items, send);
     ++*launches;
   }
   return cudaGetLastError();

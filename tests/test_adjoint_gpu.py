@@ -117,3 +117,43 @@ def test_adjoint_full_size_sampled(cuda, name):
         u = ut[int(offU[e]):int(offU[e + 1])].cpu().numpy()
         assert np.linalg.norm(g - g_ref) / np.linalg.norm(g_ref) < TOL, (name, e)
         assert np.linalg.norm(u - u_ref) / np.linalg.norm(u_ref) < TOL, (name, e)
+
+
+def test_adjoint_two_rank_slabs_bitwise_equal_one_rank(cuda):
+    """K~ and E~ over two element slabs (emulated on one GPU): each rank assembles its owned rows from S_e^T, packs
+    the S_e^T strips of shared faces for the other rank, the buffers are swapped host-side, each owner accumulates;
+    the concatenated rows equal the single-rank adjoint assembly bit for bit."""
+    import torch
+    w = gen.config("C2", nr=4, nt=10)
+    blk = gen.host_blocks(w)
+    rt = np.random.default_rng(41).standard_normal(int(np.sum(w.elem_ne)))
+
+    one = run_gpu(w, blk=blk)
+    g1, K1, E1 = one["ctx"].alloc("g"), one["ctx"].alloc("K"), one["ctx"].alloc("E")
+    one["ctx"].condense_adjoint_rhs(one["factors"], one["dev"]["B"], to_dev(rt), None, g1)
+    one["ctx"].assemble_adjoint(one["S"], g1, K1, E1)
+    reb = np.array([0, w.E // 2 - 8, w.E], dtype=np.int64)
+    rs = [run_gpu(w, blk=blk, rank=r, nranks=2, rank_elem_begin=reb) for r in range(2)]
+    offR = np.concatenate([[0], np.cumsum(np.asarray(w.elem_ne, dtype=np.int64))])
+    outs = []
+    for r in range(2):
+        me = rs[r]
+        rt_r = to_dev(rt[offR[reb[r]]:offR[reb[r + 1]]])
+        gt, Kt, Et = me["ctx"].alloc("g"), me["ctx"].alloc("K"), me["ctx"].alloc("E")
+        send = me["ctx"].alloc("send") if me["info"].send_doubles > 0 else None
+        me["ctx"].condense_adjoint_rhs(me["factors"], me["dev"]["B"], rt_r, None, gt)
+        me["ctx"].assemble_adjoint(me["S"], gt, Kt, Et, send=send)
+        outs.append((Kt, Et, send))
+    for r in range(2):
+        me, other = rs[r], rs[1 - r]
+        sc, sd, rc, rd = me["ctx"].exchange_counts()
+        osc, osd, orc, ord_ = other["ctx"].exchange_counts()
+        recv = me["ctx"].alloc("recv")
+        if rc[1 - r] > 0:
+            recv[rd[1 - r]:rd[1 - r] + rc[1 - r]] = outs[1 - r][2][osd[r]:osd[r] + osc[r]]
+        me["ctx"].skeleton_accumulate(recv, outs[r][0], outs[r][1])
+    torch.cuda.synchronize()
+    K = np.concatenate([outs[r][0].cpu().numpy()[:rs[r]["info"].nvals] for r in range(2)])
+    E = np.concatenate([outs[r][1].cpu().numpy()[:rs[r]["info"].n_owned_trace] for r in range(2)])
+    assert np.array_equal(K, K1.cpu().numpy()[:one["info"].nvals])
+    assert np.array_equal(E, E1.cpu().numpy()[:one["info"].n_owned_trace])
