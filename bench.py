@@ -46,11 +46,11 @@ def algorithmic(ne, nf):
 
 def run_adjoint(args, wl, rank, world, local):
     """The adjoint (transposed) step on the primal factors — g~ = r~_f - B^T A^-T r~_e, K~ = sum S_e^T, E~ = sum g~,
-    u~ = A^-T (r~_e - C^T lambda~) — timed like the primal step. One rank (the adjoint assembly
-    has no shared-face exchange yet)."""
+    u~ = A^-T (r~_e - C^T lambda~) — timed like the primal step (with N > 1 the S_e^T strips of
+    shared faces travel through the same transport as the primal's)."""
     import torch
-    if world > 1:
-        raise SystemExit("--path adjoint: one rank only in this version")
+    import torch.distributed as dist
+    import paper_1308_3995_b200 as hdg
     w, ctx, stream, inp, lam = wl["w"], wl["ctx"], wl["stream"], wl["inp"], wl["lam"]
     S, F, infot, K, E = (wl[k] for k in ("S", "F", "infot", "K", "E"))
     eb, n = wl["eb"], wl["n"]
@@ -68,6 +68,11 @@ def run_adjoint(args, wl, rank, world, local):
             ev[1].record(stream)
         ctx.assemble_adjoint(S, gt, K, E, send=wl["send"], stream=stream)
         launches[0] += ctx.launch_count()
+        if wl["exchange"]:
+            stream.synchronize()
+            hdg.exchange(ctx, wl["send"], wl["recv"])
+            ctx.skeleton_accumulate(wl["recv"], K, E, stream=stream)
+            launches[0] += ctx.launch_count()
         if ev:
             ev[2].record(stream)
         ctx.backsubstitute_adjoint(F, inp["C"], rt, lam_t, ut, stream=stream)
@@ -80,16 +85,23 @@ def run_adjoint(args, wl, rank, world, local):
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     clocks.start()
     launches[0] = 0
     for i in range(args.steps):
         step(evs[i])
     torch.cuda.synchronize()
     clk = clocks.stop()
-    rhs_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    asm_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    bs_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
-    ms_step = sum(e[0].elapsed_time(e[3]) for e in evs) / args.steps
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in evs), sum(e[1].elapsed_time(e[2]) for e in evs),
+                      sum(e[2].elapsed_time(e[3]) for e in evs), sum(e[0].elapsed_time(e[3]) for e in evs)],
+                     dtype=torch.float64, device=torch.device("cuda", local)) / args.steps
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    rhs_ms, asm_ms, bs_ms, ms_step = t.tolist()
     ne = np.asarray(w.elem_ne[eb:eb + n], dtype=np.float64)
     nf = np.asarray(w.elem_nf[eb:eb + n], dtype=np.float64)
     fac = 8 * ne * ne + 4 * ne
@@ -97,8 +109,9 @@ def run_adjoint(args, wl, rank, world, local):
     bs_bytes = float((fac + 8 * nf * ne + 16 * ne + 8 * nf).sum())        # factors, C, r~_e, lambda~_e, u~
     hbm = measured_peaks().get("hbm_gbs") or 6551.4
     ach = (rhs_bytes + bs_bytes) / ((rhs_ms + bs_ms) * 1e-3) / 1e9
+    elems = n if args.slab is not None else w.E
     line = {"metric": "adjoint element steps/s (fp64): adjoint rhs + K^T assembly + adjoint reconstruction",
-            "value": n / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
+            "value": elems / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "impl": "hdg", "path": "adjoint",
             "data": "synthetic (seeded Philox blocks; r~_e, lambda~ seeded stand-ins)",
