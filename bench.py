@@ -119,13 +119,22 @@ def run_adjoint(args, wl, rank, world, local):
                        "step": "condense_adjoint_rhs + assemble_adjoint + backsubstitute_adjoint"},
             "adjoint_rhs_ms": rhs_ms, "assemble_adjoint_ms": asm_ms, "backsub_adjoint_ms": bs_ms,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                         "traffic": None, "kernel": "adjoint_kernel<0, 1> (adjoint.cu)",
+                         "traffic": _traffic(args.config + "_adjoint_rhs"),
+                         "traffic_kernel": "adjoint_kernel<0> (dram read + write per launch, ncu --set full)",
+                         "kernel": "adjoint_kernel<0, 1> (adjoint.cu)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                          "bytes_per_step": rhs_bytes + bs_bytes},
             "gpu_launches": launches[0], "clocks": clk, "e2e": None, "cpu_baseline": None}
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def _traffic(key):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(key)
+    except Exception:
+        return None
 
 
 def measured_peaks():
