@@ -46,12 +46,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
     const double* Bm = a.B + a.offB[l];
     const double* re = a.re + a.offRe[l];
     // ---- T = [A | B r], row by row (consecutive lanes read consecutive entries of a row) -----------------------
-    for (int i = 0; i < ne; ++i) {
-      const double v0 = c0 < ne ? __ldg(A + i * ne + c0)
-                                : (c0 < ne + nf ? __ldg(Bm + i * nf + c0 - ne) : (c0 == ne + nf ? __ldg(re + i) : 0.0));
-      const double v1 = c1 < ne + nf ? __ldg(Bm + i * nf + c1 - ne) : (c1 == ne + nf ? __ldg(re + i) : 0.0);
-      T[i * kLdT + c0] = v0;
-      if (c1 < kLdT) T[i * kLdT + c1] = v1;
+    // (eight rows of loads in flight before their shared-memory stores: the generic T pointer could alias the
+    // global inputs as far as the compiler knows, so load/store pairs would otherwise serialise)
+    for (int i0 = 0; i0 < ne; i0 += 8) {
+      double v0[8], v1[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = i0 + q;
+        const bool rv = i < ne;
+        v0[q] = (rv && c0 < ne) ? __ldg(A + i * ne + c0)
+                                : ((rv && c0 < ne + nf) ? __ldg(Bm + i * nf + c0 - ne) : ((rv && c0 == ne + nf) ? __ldg(re + i) : 0.0));
+        v1[q] = (rv && c1 < ne + nf) ? __ldg(Bm + i * nf + c1 - ne) : ((rv && c1 == ne + nf) ? __ldg(re + i) : 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = i0 + q;
+        if (i < ne) {
+          T[i * kLdT + c0] = v0[q];
+          if (c1 < kLdT) T[i * kLdT + c1] = v1[q];
+        }
+      }
     }
     int prow = lane;   // original row now at position `lane`
     int fail = 0;
