@@ -157,3 +157,29 @@ def test_adjoint_two_rank_slabs_bitwise_equal_one_rank(cuda):
     E = np.concatenate([outs[r][1].cpu().numpy()[:rs[r]["info"].n_owned_trace] for r in range(2)])
     assert np.array_equal(K, K1.cpu().numpy()[:one["info"].nvals])
     assert np.array_equal(E, E1.cpu().numpy()[:one["info"].n_owned_trace])
+
+
+def test_adjoint_argument_errors(cuda):
+    """No plan -> HDG_ERR_STATE; null / misaligned pointers -> HDG_ERR_ARG before anything is launched."""
+    import torch
+    import paper_1308_3995_b200 as hdg
+    w = gen.config("C1", nr=2, nt=3)
+    ctx = hdg.Context(0)
+    x = torch.zeros(100000, dtype=torch.float64, device="cuda")
+    F = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    with pytest.raises(hdg.HDGError) as ei:
+        ctx.condense_adjoint_rhs(F, x, x, None, x)
+    assert ei.value.status == hdg.HDG_ERR_STATE
+    ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne)
+    with pytest.raises(hdg.HDGError) as ei:
+        ctx.condense_adjoint_rhs(F, x[1:], x, None, x)
+    assert ei.value.status == hdg.HDG_ERR_ARG
+    with pytest.raises(hdg.HDGError) as ei:
+        ctx.condense_adjoint_rhs(F, x, x, x[1:], x)
+    assert ei.value.status == hdg.HDG_ERR_ARG
+    with pytest.raises(hdg.HDGError) as ei:
+        ctx.backsubstitute_adjoint(F, x, x, None, x)
+    assert ei.value.status == hdg.HDG_ERR_ARG
+    with pytest.raises(hdg.HDGError) as ei:
+        ctx.assemble_adjoint(None, x, x, x)
+    assert ei.value.status == hdg.HDG_ERR_ARG
