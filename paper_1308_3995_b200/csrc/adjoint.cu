@@ -44,15 +44,56 @@ __device__ __forceinline__ double gemv8t(const double* M, int ld, int c0, int nc
   return __shfl_sync(0xffffffffu, acc0[0] + acc1[0], 4 * (lane & 7));
 }
 
+// Two column tiles at once: lanes 0-7 get sum_k M[k][c0 + i] v[k] (returned in .x), lanes 0-7 also get
+// sum_k M[k][c0 + 8 + i] v[k] (.y): each row contributes 16 consecutive doubles (a whole 128-byte line).
+__device__ __forceinline__ double2 gemv16t(const double* M, int ld, int c0, int ncols, int k0, int k1,
+                                           const double* v, int lane) {
+  const int gid = lane >> 2, tig = lane & 3;
+  const bool cv0 = c0 + gid < ncols, cv1 = c0 + 8 + gid < ncols;
+  double accA[2] = {0.0, 0.0}, accB[2] = {0.0, 0.0}, accC[2] = {0.0, 0.0}, accD[2] = {0.0, 0.0};
+  int k = k0;
+#pragma unroll 2
+  for (; k + 8 <= k1; k += 8) {
+    const double* r0p = M + (int64_t)(k + tig) * ld + c0 + gid;
+    const double* r1p = M + (int64_t)(k + 4 + tig) * ld + c0 + gid;
+    const double a0 = cv0 ? __ldg(r0p) : 0.0, a1 = cv1 ? __ldg(r0p + 8) : 0.0;
+    const double a2 = cv0 ? __ldg(r1p) : 0.0, a3 = cv1 ? __ldg(r1p + 8) : 0.0;
+    const double b0 = gid == 0 ? v[k + tig] : 0.0;
+    const double b1 = gid == 0 ? v[k + 4 + tig] : 0.0;
+    dmma(accA, a0, b0);
+    dmma(accB, a1, b0);
+    dmma(accC, a2, b1);
+    dmma(accD, a3, b1);
+  }
+  for (; k < k1; k += 4) {
+    const bool kv = k + tig < k1;
+    const double* rp = M + (int64_t)(k + tig) * ld + c0 + gid;
+    const double a0 = (cv0 && kv) ? __ldg(rp) : 0.0, a1 = (cv1 && kv) ? __ldg(rp + 8) : 0.0;
+    const double b0 = (gid == 0 && kv) ? v[k + tig] : 0.0;
+    dmma(accA, a0, b0);
+    dmma(accB, a1, b0);
+  }
+  const int src = 4 * (lane & 7);
+  return make_double2(__shfl_sync(0xffffffffu, accA[0] + accC[0], src), __shfl_sync(0xffffffffu, accB[0] + accD[0], src));
+}
+
 // y = A^-T x in place in vec (length ne), then the permutation into out: out[perm[i]] = y[i]
 __device__ __forceinline__ void solve_transposed(const double* LU, const int32_t* perm, int ne, double* vec,
                                                  double* out, int lane) {
   const int nt = (ne + 7) >> 3;
   const int i = lane & 7;
   // U^T v = x (forward): tile T needs U[0 .. r0, r0 .. r0+8) (upper part above the tile) and its 8x8 triangle
+  double carry = 0.0;   // tile T's GEMV from the pair pass (odd tiles)
   for (int T = 0; T < nt; ++T) {
     const int r0 = 8 * T, r = r0 + i;
-    const double s = T > 0 ? gemv8t(LU, ne, r0, ne, 0, r0, vec, lane) : 0.0;
+    double s;
+    if ((T & 1) == 0) {   // even tile: one pass over rows [0, r0) for this tile and the next
+      const double2 s2 = T > 0 ? gemv16t(LU, ne, r0, ne, 0, r0, vec, lane) : make_double2(0.0, 0.0);
+      s = s2.x;
+      carry = s2.y;
+    } else {              // odd tile: the pair pass plus the just-solved rows [r0 - 8, r0)
+      s = carry + gemv8t(LU, ne, r0, ne, r0 - 8, r0, vec, lane);
+    }
     double Uc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -68,9 +109,21 @@ __device__ __forceinline__ void solve_transposed(const double* LU, const int32_t
     __syncwarp();
   }
   // L^T y = v (backward, unit diagonal): tile T needs L[r0+8 .. ne, r0 .. r0+8) (below the tile)
+  bool have = false;   // carry holds tile T's GEMV over rows >= r0 + 16 from the pair pass
   for (int T = nt - 1; T >= 0; --T) {
     const int r0 = 8 * T, r = r0 + i, rend = min(r0 + 8, ne);
-    const double s = rend < ne ? gemv8t(LU, ne, r0, ne, rend, ne, vec, lane) : 0.0;
+    double s;
+    if (have) {           // second tile of a pair: add the just-solved rows [rend, rend + 8)
+      s = carry + gemv8t(LU, ne, r0, ne, rend, min(rend + 8, ne), vec, lane);
+      have = false;
+    } else if (T > 0) {   // first tile of a pair: one pass over rows [rend, ne) for tiles T - 1 and T
+      const double2 s2 = rend < ne ? gemv16t(LU, ne, r0 - 8, ne, rend, ne, vec, lane) : make_double2(0.0, 0.0);
+      s = s2.y;
+      carry = s2.x;
+      have = true;
+    } else {
+      s = rend < ne ? gemv8t(LU, ne, r0, ne, rend, ne, vec, lane) : 0.0;
+    }
     double Lc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -116,10 +169,11 @@ __global__ void __launch_bounds__(kWarps * 32) adjoint_kernel(const AdjointArgs 
       const double* Bm = a.M + a.offM[l];
       double* gt = a.out + a.offOut[l];
       const double* rf = a.rf ? a.rf + a.offRf[l] : nullptr;
-      for (int c0 = 0; c0 < nf; c0 += 8) {
-        const double s = gemv8t(Bm, nf, c0, nf, 0, ne, z, lane);
+      for (int c0 = 0; c0 < nf; c0 += 16) {
+        const double2 s = gemv16t(Bm, nf, c0, nf, 0, ne, z, lane);
         const int c = c0 + lane;
-        if (lane < 8 && c < nf) gt[c] = (rf ? __ldg(rf + c) : 0.0) - s;
+        if (lane < 8 && c < nf) gt[c] = (rf ? __ldg(rf + c) : 0.0) - s.x;
+        if (lane < 8 && c + 8 < nf) gt[c + 8] = (rf ? __ldg(rf + c + 8) : 0.0) - s.y;
       }
     } else {
       // lambda~_e in slot order (the element's faces, each face's dofs in face_off order), zero padded
