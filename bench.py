@@ -18,6 +18,7 @@ GPU, element slabs, NCCL for the shared-face exchange). Rank 0 prints ONE JSON l
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import subprocess
@@ -80,15 +81,16 @@ def run_adjoint(args, wl, rank, world, local):
         if ev:
             ev[3].record(stream)
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark()
     launches[0] = 0
     for i in range(args.steps):
         step(evs[i])
@@ -168,7 +170,10 @@ class ClockSampler:
         self.path = os.path.join("/tmp", f"hdg_clocks_{os.getpid()}.csv")
 
     def start(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        """Started before the warm-up (nvidia-smi needs ~0.1-0.3 s to produce its first sample); mark() / stop()
+        bracket the timed region and only samples inside it are kept (all of them if the region was too short)."""
+        self.t_mark = None
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
@@ -178,7 +183,11 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def mark(self):
+        self.t_mark = time.time()
+
     def stop(self):
+        t_end = time.time()
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -189,17 +198,26 @@ class ClockSampler:
         rows = []
         for line in open(self.path):
             f = [x.strip() for x in line.split(",")]
-            if len(f) >= 9:
+            if len(f) >= 10:
                 try:
-                    rows.append((float(f[1]), float(f[2]), f[5:9]))
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
                 except ValueError:
                     pass
         if not rows:
-            return {"samples": 0, "note": "timed region shorter than nvidia-smi's first 100 ms sample"}
+            return {"samples": 0, "note": "no nvidia-smi sample"}
+        inside = [r for r in rows if self.t_mark is not None and self.t_mark - 0.05 <= r[0] <= t_end + 0.05]
+        note = None
+        if not inside:
+            inside = rows[-3:]
+            note = "timed region shorter than the 100 ms sampling interval: last samples of the warm-up and region"
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i in range(4) if r[i].lower() == "active"})
-        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": max(r[1] for r in rows),
-                "samples": len(rows), "reasons": reasons}
+        reasons = sorted({names[i] for _, _, _, r in inside for i in range(4) if r[i].lower() == "active"})
+        out = {"sm_mhz": float(np.median([r[1] for r in inside])), "sm_max_mhz": max(r[2] for r in inside),
+               "samples": len(inside), "reasons": reasons}
+        if note:
+            out["note"] = note
+        return out
 
 
 def slab_bounds(E: int, n: int):
@@ -400,6 +418,8 @@ def main():
                 flush.fill_(1.0)
         launches[0] += run_step(wl, ev)
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -409,11 +429,10 @@ def main():
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark()
     launches[0] = 0
     t0.record(stream)
     for i in range(args.steps):
