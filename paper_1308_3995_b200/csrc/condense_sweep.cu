@@ -892,9 +892,9 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
             const Region R1b(nextr_hi, RA, jn, NC);
             const Region R2(0, G.NF8, jn, CB);
             const int tot = R1a.nblk + R1b.nblk + R2.nblk;
-            // trailing blocks: the 6 MMA workers, plus the helper in the first half of the panels (there the
+            // trailing blocks: the 6 MMA workers, plus the helper in the first two thirds of the panels (there the
             // workers bound the step; later the chain warp does, and it shares the helper's SMSP tensor pipe)
-            const bool hjoin = 2 * p < G.npan;
+            const bool hjoin = 3 * p < 2 * G.npan;   // (first 2/3: C4 38.7 -> 38.4 ms vs the first half)
             const int nt_w = hjoin ? NWK + 1 : NWK;
             const int tw = helper ? (hjoin ? NWK : 1 << 30) : w;
             for (int b = (a.debug & 1) ? 1 << 30 : tw; b < tot; b += nt_w) {
