@@ -201,6 +201,10 @@ def test_empty_slab(cuda):
     ctx.condense(t, t, t, t, t, t, t, t, ctx.alloc("factors"), ctx.alloc("info"))
     ctx.assemble_skeleton(t, t, ctx.alloc("K"), ctx.alloc("E"))
     ctx.backsubstitute(ctx.alloc("factors"), t, t, t, t)
+    # the adjoint calls on the empty slab are no-ops too
+    ctx.condense_adjoint_rhs(ctx.alloc("factors"), t, t, None, t)
+    ctx.assemble_adjoint(t, t, ctx.alloc("K"), ctx.alloc("E"))
+    ctx.backsubstitute_adjoint(ctx.alloc("factors"), t, t, t, t)
 
 
 def test_deterministic(cuda):
