@@ -135,12 +135,19 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs a) {
     ++ns;
   }
   double* dst = a.K + a.blk_off[q];
+  int r = lane / nb, cc = lane - (lane / nb) * nb;   // (r, cc) of idx, advanced by 32 without divisions
+  const int step_r = 32 / nb, step_c = 32 - (32 / nb) * nb;
   for (int idx = lane; idx < na * nb; idx += 32) {
-    const int r = idx / nb, cc = idx - r * nb;
     double v = 0.0;
     if (ns > 0) v = v + __ldg(TR ? src[0] + (int64_t)cc * ld[0] + r : src[0] + (int64_t)r * ld[0] + cc);
     if (ns > 1) v = v + __ldg(TR ? src[1] + (int64_t)cc * ld[1] + r : src[1] + (int64_t)r * ld[1] + cc);
     dst[idx] = v;
+    r += step_r;
+    cc += step_c;
+    if (cc >= nb) {
+      cc -= nb;
+      ++r;
+    }
   }
 }
 
