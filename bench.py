@@ -69,9 +69,8 @@ def run_adjoint(args, wl, rank, world, local):
             ev[1].record(stream)
         ctx.assemble_adjoint(S, gt, K, E, send=wl["send"], stream=stream)
         launches[0] += ctx.launch_count()
-        if wl["exchange"]:
-            stream.synchronize()
-            hdg.exchange(ctx, wl["send"], wl["recv"])
+        if wl["exchange"] and not ctx.has_comm:   # (with its own communicator the library exchanged already)
+            hdg.exchange(ctx, wl["send"], wl["recv"], stream=stream)
             ctx.skeleton_accumulate(wl["recv"], K, E, stream=stream)
             launches[0] += ctx.launch_count()
         if ev:
@@ -302,7 +301,9 @@ def setup_workload(config: str, rank: int = 0, world: int = 1, local: int = 0, s
     else:
         reb = slab_bounds(w.E, world)
         eb, n = int(reb[rank]), int(reb[rank + 1] - reb[rank])
-        ctx = hdg.Context(local, rank, world)
+        # N > 1: the context owns an NCCL communicator; hdg_assemble_skeleton packs, exchanges (grouped
+        # ncclSend/ncclRecv on the step's stream) and accumulates the shared-face rows itself
+        ctx = hdg.nccl_context(local, rank, world) if world > 1 else hdg.Context(local, rank, world)
         info = ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne, eb, n, reb if world > 1 else None)
     stream = torch.cuda.Stream(dev)
     inp = {}
@@ -323,8 +324,9 @@ def setup_workload(config: str, rank: int = 0, world: int = 1, local: int = 0, s
                exchange=(world > 1 and slab is None))
     for k in ("S", "g", "u", "factors", "info", "K", "E"):
         out[{"factors": "F", "info": "infot"}.get(k, k)] = ctx.alloc(k)
-    out["send"] = ctx.alloc("send") if info.send_doubles > 0 else None
-    out["recv"] = ctx.alloc("recv") if info.recv_doubles > 0 else None
+    own = ctx.has_comm
+    out["send"] = ctx.alloc("send") if info.send_doubles > 0 and not own else None
+    out["recv"] = ctx.alloc("recv") if info.recv_doubles > 0 and not own else None
     return out
 
 
@@ -342,9 +344,8 @@ def run_step(wl, ev=None):
         ev[1].record(stream)
     ctx.assemble_skeleton(wl["S"], wl["g"], wl["K"], wl["E"], send=wl["send"], stream=stream)
     n += ctx.launch_count()
-    if wl["exchange"]:
-        stream.synchronize()
-        hdg.exchange(ctx, wl["send"], wl["recv"])
+    if wl["exchange"] and not ctx.has_comm:   # (with its own communicator the library exchanged already)
+        hdg.exchange(ctx, wl["send"], wl["recv"], stream=stream)
         ctx.skeleton_accumulate(wl["recv"], wl["K"], wl["E"], stream=stream)
         n += ctx.launch_count()
     if ev:
@@ -542,7 +543,8 @@ def main():
             "data": "synthetic (seeded Philox blocks with BASELINE.json distributions, generated in HBM)",
             "config": {"workload": workload, "elements": elems, "n_e": int(w.elem_ne[eb:eb + n].max()),
                        "n_f": int(w.elem_nf[eb:eb + n].max()), "faces": w.F, "trace_dofs": w.n_trace,
-                       "parallelism": f"element slabs x{world}" + (" + NCCL shared-face exchange" if world > 1 else ""),
+                       "parallelism": f"element slabs x{world}" + (" + NCCL shared-face exchange inside "
+                                                                   "hdg_assemble_skeleton" if world > 1 else ""),
                        "l2": ("inputs (%.1f GB/rank) exceed the 126 MB L2; no flush needed" % (in_bytes / 1e9)
                               if flush is None else
                               "inputs (%.3f GB/rank) under 4x the 126 MB L2: a 512 MB buffer is written before every timed step, "

@@ -53,7 +53,8 @@ typedef enum {
   HDG_ERR_CUDA = 3,        /* CUDA runtime error (message in hdg_last_error) */
   HDG_ERR_NOMEM = 4,       /* workspace allocation failed */
   HDG_ERR_STATE = 5,       /* call out of order (e.g. compute before hdg_plan) */
-  HDG_ERR_UNSUPPORTED = 6  /* sizes outside what this build supports (n_e > 256, n_f > 96, ...) */
+  HDG_ERR_UNSUPPORTED = 6, /* sizes outside what this build supports (n_e > 256, n_f > 96, ...) */
+  HDG_ERR_NCCL = 7         /* NCCL unavailable or an NCCL call failed (message in hdg_last_error / stderr) */
 } hdg_status;
 
 /* Library version and the supported maxima. */
@@ -63,9 +64,22 @@ int hdg_max_face_ndof(void);   /* largest n_f (element trace size) supported */
 
 const char* hdg_status_string(hdg_status s);
 
+/* a7 bootstrap: a fresh NCCL unique id ([host] 128 bytes), generated on ONE rank (rank 0) and
+ * distributed to the others by the caller (e.g. torch.distributed broadcast). NCCL is loaded at run time
+ * (libnccl.so.2); HDG_ERR_NCCL if it is unavailable. */
+hdg_status hdg_get_unique_id(unsigned char id[128]);
+
 /* Context on CUDA device `device` for rank `rank` of `nranks` (element-slab partition; see hdg_mesh).
- * [host] out. The context owns the plan and all workspace. */
-hdg_status hdg_ctx_create(hdg_ctx* out, int device, int rank, int nranks);
+ * [host] out. The context owns the plan and all workspace.
+ * nccl_id [host, 128 bytes]: NULL for a single rank, or for nranks > 1 when the caller transports the exchange
+ * buffers itself (hdg_exchange_counts / hdg_skeleton_accumulate). Non-NULL: every rank passes the same id from
+ * hdg_get_unique_id and the call creates the context's NCCL communicator (ncclCommInitRank: collective, blocks
+ * until all nranks ranks have called it); hdg_assemble_skeleton / hdg_assemble_adjoint then perform the
+ * shared-face exchange themselves, stream-ordered. Errors: HDG_ERR_ARG (bad rank/nranks), HDG_ERR_CUDA (device),
+ * HDG_ERR_UNSUPPORTED (not compute capability 10.x), HDG_ERR_NCCL (communicator). */
+hdg_status hdg_ctx_create(hdg_ctx* out, int device, int rank, int nranks, const unsigned char* nccl_id);
+/* 1 if the context owns an NCCL communicator (created with an id), else 0. */
+int hdg_ctx_has_comm(hdg_ctx ctx);
 void hdg_ctx_destroy(hdg_ctx ctx);
 const char* hdg_last_error(hdg_ctx ctx);
 
@@ -123,8 +137,14 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
  * counts, 0-based), col_idx [nnzb] int32 global face ids ascending (diagonal included), blk_off [nnzb + 1]
  * int64 offsets of each row-major n_fp(row) x n_fp(col) block in K (doubles), K [nvals], E [n_owned_trace].
  * row_ptr/col_idx/blk_off may be NULL (structure not copied out; it is fixed by the plan).
- * With nranks > 1, send (device, plan.send_doubles) receives this rank's contributions to face rows owned by
- * other ranks; exchange it with hdg_exchange_counts' layout and finish with hdg_skeleton_accumulate. */
+ * a7, nranks > 1: the right (non-owner) element's contributions to a shared face row travel to
+ * the row's owner and are added AFTER the owner's own, so K and E are bitwise those of one rank (P12).
+ *   - context with an NCCL communicator: this call packs them into library-owned buffers, exchanges them with
+ *     one grouped ncclSend/ncclRecv on `stream` and accumulates them, all stream-ordered (no host sync); `send`
+ *     is ignored (may be NULL).
+ *   - context without one: send (device, plan.send_doubles) receives this rank's contributions to face rows
+ *     owned by other ranks; the caller exchanges it with hdg_exchange_counts' layout (on the same stream order)
+ *     and finishes with hdg_skeleton_accumulate. */
 hdg_status hdg_assemble_skeleton(hdg_ctx ctx, const double* S, const double* g, int32_t* row_ptr,
                                  int32_t* col_idx, int64_t* blk_off, double* K, double* E, double* send,
                                  hdg_stream stream);
@@ -170,9 +190,11 @@ hdg_status hdg_condense_adjoint_rhs(hdg_ctx ctx, const void* factors, const doub
 
 /* Adjoint skeleton assembly: Kt = sum_e S_e^T (= K^T block by block) into the plan's block-CSR
  * structure (same row_ptr / col_idx / blk_off as hdg_assemble_skeleton), Et = sum_e g~_e, left then right.
- * S from hdg_condense, gt from hdg_condense_adjoint_rhs. With nranks > 1, send (plan.send_doubles, device) receives
- * this rank's contributions to rows owned by others (strips of S_e^T, same layout as hdg_assemble_skeleton's);
- * after the transport, hdg_skeleton_accumulate(recv, Kt, Et) finishes the owned rows (bitwise as one rank). */
+ * S from hdg_condense, gt from hdg_condense_adjoint_rhs. With nranks > 1 the exchange is as for
+ * hdg_assemble_skeleton: inside the call when the context has an NCCL communicator; otherwise send
+ * (plan.send_doubles, device) receives this rank's contributions to rows owned by others (strips of S_e^T, same
+ * layout) and, after the caller's transport, hdg_skeleton_accumulate(recv, Kt, Et) finishes the owned rows
+ * (bitwise as one rank). */
 hdg_status hdg_assemble_adjoint(hdg_ctx ctx, const double* S, const double* gt, double* Kt, double* Et,
                                 double* send, hdg_stream stream);
 

@@ -23,7 +23,7 @@
 
 /* ---------------------------------------------------------------------------------------------------------
  * O1 factor: P A = L U in place (row-major n x n), LAPACK getrf conventions: piv[k] = row swapped with k.
- * Returns 0, or k+1 if the k-th pivot is exactly zero. */
+ * Returns 0, or k+1 if the k-th pivot is exactly zero or NaN (R7: NaN pivots fail too). */
 int oracle_lu(int n, double* a, int32_t* piv) {
   for (int k = 0; k < n; ++k) {
     int p = k;
@@ -33,7 +33,7 @@ int oracle_lu(int n, double* a, int32_t* piv) {
       if (v > best) { best = v; p = i; }            /* strict '>' : first index on ties */
     }
     piv[k] = p;
-    if (a[(int64_t)p * n + k] == 0.0) return k + 1;
+    if (a[(int64_t)p * n + k] == 0.0 || a[(int64_t)p * n + k] != a[(int64_t)p * n + k]) return k + 1;
     if (p != k)
       for (int j = 0; j < n; ++j) {
         const double t = a[(int64_t)k * n + j];

@@ -21,7 +21,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhdg.so")
 
-HDG_OK, HDG_ERR_ARG, HDG_ERR_SINGULAR, HDG_ERR_CUDA, HDG_ERR_NOMEM, HDG_ERR_STATE, HDG_ERR_UNSUPPORTED = range(7)
+(HDG_OK, HDG_ERR_ARG, HDG_ERR_SINGULAR, HDG_ERR_CUDA, HDG_ERR_NOMEM, HDG_ERR_STATE, HDG_ERR_UNSUPPORTED,
+ HDG_ERR_NCCL) = range(8)
 
 
 class HDGError(RuntimeError):
@@ -62,7 +63,11 @@ def lib():
         L.hdg_status_string.restype = ctypes.c_char_p
         L.hdg_status_string.argtypes = [I32]
         L.hdg_ctx_create.restype = I32
-        L.hdg_ctx_create.argtypes = [ctypes.POINTER(P), I32, I32, I32]
+        L.hdg_ctx_create.argtypes = [ctypes.POINTER(P), I32, I32, I32, P]
+        L.hdg_get_unique_id.restype = I32
+        L.hdg_get_unique_id.argtypes = [P]
+        L.hdg_ctx_has_comm.restype = I32
+        L.hdg_ctx_has_comm.argtypes = [P]
         L.hdg_ctx_destroy.argtypes = [P]
         L.hdg_last_error.restype = ctypes.c_char_p
         L.hdg_last_error.argtypes = [P]
@@ -98,7 +103,8 @@ def lib():
     return _lib
 
 
-EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status_string", "hdg_ctx_create",
+EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status_string", "hdg_get_unique_id",
+            "hdg_ctx_create", "hdg_ctx_has_comm",
             "hdg_ctx_destroy", "hdg_last_error", "hdg_plan", "hdg_condense", "hdg_assemble_skeleton",
             "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
             "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout", "hdg_condense_adjoint_rhs",
@@ -159,17 +165,34 @@ class PlanInfo:
     recv_doubles: int
 
 
-class Context:
-    """One libhdg context (device, rank of nranks). Mirrors include/hdg.h call for call."""
+def get_unique_id() -> bytes:
+    """hdg_get_unique_id: a fresh 128-byte NCCL id (call on one rank, distribute to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().hdg_get_unique_id(buf)
+    if st != HDG_OK:
+        raise HDGError(st, "hdg_get_unique_id: NCCL unavailable")
+    return buf.raw
 
-    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1):
+
+class Context:
+    """One libhdg context (device, rank of nranks). Mirrors include/hdg.h call for call.
+    nccl_id (128 bytes from get_unique_id, the same on every rank): the context creates its own NCCL communicator
+    and hdg_assemble_skeleton / hdg_assemble_adjoint perform the shared-face exchange inside the call."""
+
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None):
         self._L = lib()
         h = ctypes.c_void_p()
-        st = self._L.hdg_ctx_create(ctypes.byref(h), device, rank, nranks)
+        idbuf = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be 128 bytes")
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        st = self._L.hdg_ctx_create(ctypes.byref(h), device, rank, nranks, idbuf)
         if st != HDG_OK:
             raise HDGError(st, f"hdg_ctx_create(device={device}): {self._L.hdg_status_string(st).decode()}")
         self._h = h
         self.device, self.rank, self.nranks = device, rank, nranks
+        self.has_comm = bool(self._L.hdg_ctx_has_comm(h))
         self.info: PlanInfo | None = None
         self._keep = None
 
@@ -342,7 +365,25 @@ def exchange_buffers(send, recv, send_counts, send_displs, recv_counts, recv_dis
             w.wait()
 
 
-def exchange(ctx: Context, send, recv, group=None):
-    """a7 transport for a planned context (counts from hdg_exchange_counts)."""
+def exchange(ctx: Context, send, recv, group=None, stream=None):
+    """a7 transport for a planned context without its own communicator (counts from hdg_exchange_counts), issued
+    on `stream` (torch's NCCL ops order themselves after, and the stream after, the current stream). A context
+    with an NCCL communicator exchanges inside hdg_assemble_* and this is a no-op."""
+    if ctx.has_comm:
+        return
+    import torch
     sc, sd, rc, rd = ctx.exchange_counts()
-    exchange_buffers(send, recv, sc, sd, rc, rd, ctx.rank, ctx.nranks, group)
+    if stream is not None and send is not None and send.is_cuda:
+        with torch.cuda.stream(stream):
+            exchange_buffers(send, recv, sc, sd, rc, rd, ctx.rank, ctx.nranks, group)
+    else:
+        exchange_buffers(send, recv, sc, sd, rc, rd, ctx.rank, ctx.nranks, group)
+
+
+def nccl_context(device: int, rank: int, nranks: int, group=None) -> Context:
+    """Context with its own NCCL communicator, bootstrapped over an initialised torch.distributed group: rank 0
+    draws the id (hdg_get_unique_id) and broadcasts it (plumbing only)."""
+    import torch.distributed as dist
+    obj = [get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return Context(device, rank, nranks, nccl_id=obj[0])

@@ -7,7 +7,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libhdg.so")
-SOURCES = ["api.cu", "condense.cu", "condense_sweep.cu", "condense_warp.cu", "backsub.cu", "skeleton.cu", "adjoint.cu"]
+SOURCES = ["api.cu", "condense.cu", "condense_sweep.cu", "condense_warp.cu", "backsub.cu", "skeleton.cu", "adjoint.cu",
+           "comm.cu"]
 HEADERS = ["hdg_internal.cuh", "dev_common.cuh", os.path.join("..", "..", "include", "hdg.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
@@ -24,19 +25,25 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return SO
-    objs = []
+    # the translation units compile in parallel (the sweep/panel kernels dominate: ~2 min serially)
+    jobs = []
     for s in SOURCES:
         o = os.path.join(CSRC, s.replace(".cu", ".o"))
         cmd = ["nvcc", *NVCC_FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if verbose or r.returncode:
+        jobs.append((s, o, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    objs, failed = [], []
+    for s, o, cmd, pr in jobs:
+        out, err = pr.communicate()
+        if verbose or pr.returncode:
             print(" ".join(cmd))
-            print(r.stdout, r.stderr)
-        if r.returncode:
-            raise RuntimeError(f"nvcc failed on {s}")
+            print(out, err)
+        if pr.returncode:
+            failed.append(s)
         objs.append(o)
+    if failed:
+        raise RuntimeError(f"nvcc failed on {failed}")
     tmp = SO + ".tmp"
-    cmd = ["nvcc", "-shared", "-o", tmp, *objs, "-lcudart"]
+    cmd = ["nvcc", "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"]   # NCCL: dlopen at run time (comm.cu)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         print(r.stdout, r.stderr)

@@ -12,6 +12,14 @@
 
 using namespace hdg;
 
+int64_t hdg::grid_cap(int64_t grid) {
+  static const int64_t cap = [] {
+    const char* v = getenv("HDG_MAX_GRID");
+    return v ? std::max<int64_t>(1, atoll(v)) : (int64_t)0;
+  }();
+  return cap > 0 && grid > cap ? cap : grid;
+}
+
 namespace {
 
 const char* kVersion = "libhdg 0.1 (sm_100a, fp64)";
@@ -54,6 +62,7 @@ void free_plan(Plan& p) {
   cudaFree(p.sk.d_row_ptr); cudaFree(p.sk.d_col_idx); cudaFree(p.sk.d_blk_off); cudaFree(p.sk.d_blk_row);
   cudaFree(p.sk.d_send_items); cudaFree(p.sk.d_recv_items);
   cudaFree(p.d_scratch);
+  cudaFree(p.d_send); cudaFree(p.d_recv);
   p = Plan();
 }
 
@@ -133,6 +142,24 @@ void build_exchange_layout(const hdg_mesh* m, int rank, int R, ExchangeLayout& x
   }
 }
 
+// a6 (+ a7): assemble the owned rows and pack contributions to rows owned by other ranks; with an NCCL
+// communicator the exchange and the ordered accumulate follow on the same stream (no host sync). Without one the
+// caller transports `send` and finishes with hdg_skeleton_accumulate (the three-call protocol).
+hdg_status assemble_and_exchange(hdg_ctx ctx, const double* S, const double* g, double* K, double* E, double* send,
+                                 cudaStream_t s, bool transposed, const char* name) {
+  const Plan& p = ctx->plan;
+  const bool lib_x = ctx->nccl_comm && ctx->nranks > 1;
+  double* sbuf = lib_x ? p.d_send : send;
+  HDG_CUDA(ctx, launch_assemble(p, S, g, K, E, sbuf, s, &ctx->launches, transposed));
+  if (lib_x) {
+    std::string err;
+    if (!nccl_exchange(ctx->nccl_comm, p, ctx->rank, ctx->nranks, p.d_send, p.d_recv, s, &err))
+      return fail(ctx, HDG_ERR_NCCL, "%s: %s", name, err.c_str());
+    HDG_CUDA(ctx, launch_accumulate(p, p.d_recv, K, E, s, &ctx->launches));
+  }
+  return HDG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -150,11 +177,22 @@ const char* hdg_status_string(hdg_status s) {
     case HDG_ERR_NOMEM: return "out of memory";
     case HDG_ERR_STATE: return "invalid state";
     case HDG_ERR_UNSUPPORTED: return "unsupported size";
+    case HDG_ERR_NCCL: return "NCCL error";
   }
   return "unknown status";
 }
 
-hdg_status hdg_ctx_create(hdg_ctx* out, int device, int rank, int nranks) {
+hdg_status hdg_get_unique_id(unsigned char id[128]) {
+  if (!id) return HDG_ERR_ARG;
+  std::string err;
+  if (!nccl_unique_id(id, &err)) {
+    std::fprintf(stderr, "hdg_get_unique_id: %s\n", err.c_str());
+    return HDG_ERR_NCCL;
+  }
+  return HDG_OK;
+}
+
+hdg_status hdg_ctx_create(hdg_ctx* out, int device, int rank, int nranks, const unsigned char* nccl_id) {
   if (!out || nranks < 1 || rank < 0 || rank >= nranks) return HDG_ERR_ARG;
   *out = nullptr;
   int ndev = 0;
@@ -169,14 +207,25 @@ hdg_status hdg_ctx_create(hdg_ctx* out, int device, int rank, int nranks) {
   c->nranks = nranks;
   c->sms = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
+  if (nccl_id) {
+    std::string err;
+    if (!nccl_comm_init(&c->nccl_comm, nranks, rank, nccl_id, &err)) {
+      std::fprintf(stderr, "hdg_ctx_create: %s\n", err.c_str());
+      delete c;
+      return HDG_ERR_NCCL;
+    }
+  }
   *out = c;
   return HDG_OK;
 }
+
+int hdg_ctx_has_comm(hdg_ctx ctx) { return ctx && ctx->nccl_comm ? 1 : 0; }
 
 void hdg_ctx_destroy(hdg_ctx ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   free_plan(ctx->plan);
+  nccl_comm_destroy(ctx->nccl_comm);
   delete ctx;
 }
 
@@ -203,6 +252,9 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     if (m->rank_elem_begin[ctx->rank] != eb || m->rank_elem_begin[ctx->rank + 1] != eb + n ||
         m->rank_elem_begin[0] != 0 || m->rank_elem_begin[ctx->nranks] != E)
       return fail(ctx, HDG_ERR_ARG, "hdg_plan: rank_elem_begin inconsistent with elem_begin/n_elem");
+    for (int r = 0; r < ctx->nranks; ++r)
+      if (m->rank_elem_begin[r + 1] < m->rank_elem_begin[r])
+        return fail(ctx, HDG_ERR_ARG, "hdg_plan: rank_elem_begin is not non-decreasing at rank %d", r);
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   HDG_CUDA(ctx, cudaSetDevice(ctx->device));
@@ -218,6 +270,15 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     const int32_t nd = m->face_ndof[f];
     if (nd <= 0 || (nd & 1)) return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_plan: face %lld trace size %d (must be even, > 0)", (long long)f, nd);
   }
+  // every element's slots (remote neighbours too: the symbolic structure, the exchange layout and the
+  // accumulate kernel index face_ndof / col_idx through them), and the faces' back-references
+  for (int64_t e = 0; e < E; ++e)
+    for (int k = 0; k < 3; ++k) {
+      const int32_t f = m->elem_face[3 * e + k];
+      if (f < -1 || f >= F) return fail(ctx, HDG_ERR_ARG, "hdg_plan: element %lld slot %d face %d out of range", (long long)e, k, f);
+      if (f >= 0 && m->face_elem[2 * f] != e && m->face_elem[2 * f + 1] != e)
+        return fail(ctx, HDG_ERR_ARG, "hdg_plan: element %lld lists face %d which does not list it", (long long)e, f);
+    }
   std::vector<int64_t> face_off(F + 1, 0);
   for (int64_t f = 0; f < F; ++f) face_off[f + 1] = face_off[f] + m->face_ndof[f];
   p.n_trace = face_off[F];
@@ -318,7 +379,11 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
   HDG_CUDA(ctx, upload(&p.d_ne, ne.data(), (size_t)n));
   HDG_CUDA(ctx, upload(&p.d_nf, nf.data(), (size_t)n));
   for (int k = 0; k < 10; ++k) HDG_CUDA(ctx, upload(&p.d_off[k], off[k].data(), (size_t)(n + 1)));
-  HDG_CUDA(ctx, skeleton_symbolic(p, s));
+  {
+    const cudaError_t e = skeleton_symbolic(p, s);
+    if (e == cudaErrorMemoryAllocation) return fail(ctx, HDG_ERR_NOMEM, "hdg_plan: block-CSR structure: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "hdg_plan: skeleton_symbolic");
+  }
 
   // ---- exchange lists (faces shared between slabs) ----------------------------------------------------------------
   const int R = ctx->nranks;
@@ -332,6 +397,11 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     p.sk.n_recv_items = (int64_t)x.recv_items.size() / 3;
     HDG_CUDA(ctx, upload(&p.sk.d_send_items, x.send_items.data(), x.send_items.size()));
     HDG_CUDA(ctx, upload(&p.sk.d_recv_items, x.recv_items.data(), x.recv_items.size()));
+    if (ctx->nccl_comm) {   // the library owns the exchange buffers (a7 runs inside hdg_assemble_*)
+      if (cudaMalloc(&p.d_send, sizeof(double) * std::max<int64_t>(1, x.send_doubles)) != cudaSuccess ||
+          cudaMalloc(&p.d_recv, sizeof(double) * std::max<int64_t>(1, x.recv_doubles)) != cudaSuccess)
+        return fail(ctx, HDG_ERR_NOMEM, "hdg_plan: exchange buffers");
+    }
   } else {
     p.sk.send_counts.assign(1, 0); p.sk.send_displs.assign(1, 0);
     p.sk.recv_counts.assign(1, 0); p.sk.recv_displs.assign(1, 0);
@@ -396,15 +466,15 @@ hdg_status hdg_assemble_skeleton(hdg_ctx ctx, const double* S, const double* g, 
   ctx->launches = 0;
   if ((p.sk.nvals > 0 && !K) || (p.sk.ntr > 0 && !E) || (p.n > 0 && (!S || !g)))
     return fail(ctx, HDG_ERR_ARG, "hdg_assemble_skeleton: null pointer");
-  if (p.sk.send_doubles > 0 && !send) return fail(ctx, HDG_ERR_ARG, "hdg_assemble_skeleton: send buffer required");
+  if (p.sk.send_doubles > 0 && !send && !ctx->nccl_comm)
+    return fail(ctx, HDG_ERR_ARG, "hdg_assemble_skeleton: send buffer required");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   HDG_CUDA(ctx, cudaSetDevice(ctx->device));
   const int64_t nrows = p.sk.f1 - p.sk.f0;
   if (row_ptr) HDG_CUDA(ctx, cudaMemcpyAsync(row_ptr, p.sk.d_row_ptr, sizeof(int32_t) * (nrows + 1), cudaMemcpyDeviceToDevice, s));
   if (col_idx && p.sk.nnzb) HDG_CUDA(ctx, cudaMemcpyAsync(col_idx, p.sk.d_col_idx, sizeof(int32_t) * p.sk.nnzb, cudaMemcpyDeviceToDevice, s));
   if (blk_off) HDG_CUDA(ctx, cudaMemcpyAsync(blk_off, p.sk.d_blk_off, sizeof(int64_t) * (p.sk.nnzb + 1), cudaMemcpyDeviceToDevice, s));
-  HDG_CUDA(ctx, launch_assemble(p, S, g, K, E, send, s, &ctx->launches));
-  return HDG_OK;
+  return assemble_and_exchange(ctx, S, g, K, E, send, s, false, "hdg_assemble_skeleton");
 }
 
 hdg_status hdg_exchange_counts(hdg_ctx ctx, int64_t* send_counts, int64_t* send_displs, int64_t* recv_counts,
@@ -509,11 +579,11 @@ hdg_status hdg_assemble_adjoint(hdg_ctx ctx, const double* S, const double* gt, 
   ctx->launches = 0;
   if ((p.sk.nvals > 0 && !Kt) || (p.sk.ntr > 0 && !Et) || (p.n > 0 && (!S || !gt)))
     return fail(ctx, HDG_ERR_ARG, "hdg_assemble_adjoint: null pointer");
-  if (p.sk.send_doubles > 0 && !send) return fail(ctx, HDG_ERR_ARG, "hdg_assemble_adjoint: send buffer required");
+  if (p.sk.send_doubles > 0 && !send && !ctx->nccl_comm)
+    return fail(ctx, HDG_ERR_ARG, "hdg_assemble_adjoint: send buffer required");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   HDG_CUDA(ctx, cudaSetDevice(ctx->device));
-  HDG_CUDA(ctx, launch_assemble(p, S, gt, Kt, Et, send, s, &ctx->launches, true));
-  return HDG_OK;
+  return assemble_and_exchange(ctx, S, gt, Kt, Et, send, s, true, "hdg_assemble_adjoint");
 }
 
 hdg_status hdg_first_error(hdg_ctx ctx, const int32_t* info, int64_t* elem, int32_t* code, hdg_stream stream) {
@@ -549,6 +619,16 @@ hdg_status hdg_exchange_layout(const hdg_mesh* m, int rank, int nranks, int64_t*
     return HDG_ERR_ARG;
   if (m->rank_elem_begin[rank] != m->elem_begin || m->rank_elem_begin[rank + 1] != m->elem_begin + m->n_elem)
     return HDG_ERR_ARG;
+  const int64_t E = m->n_elem_global, F = m->n_face;
+  if (m->rank_elem_begin[0] != 0 || m->rank_elem_begin[nranks] != E) return HDG_ERR_ARG;
+  for (int r = 0; r < nranks; ++r)
+    if (m->rank_elem_begin[r + 1] < m->rank_elem_begin[r]) return HDG_ERR_ARG;
+  for (int64_t i = 0; i < 3 * E; ++i)
+    if (m->elem_face[i] < -1 || m->elem_face[i] >= F) return HDG_ERR_ARG;
+  for (int64_t f = 0; f < F; ++f) {
+    const int32_t l = m->face_elem[2 * f], r = m->face_elem[2 * f + 1];
+    if (l < 0 || l >= E || r >= E || (r >= 0 && r <= l) || m->face_ndof[f] <= 0) return HDG_ERR_ARG;
+  }
   ExchangeLayout x;
   build_exchange_layout(m, rank, nranks, x);
   for (int r = 0; r < nranks; ++r) {

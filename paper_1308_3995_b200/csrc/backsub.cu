@@ -20,9 +20,10 @@ namespace {
 constexpr int kWarps = 8;
 
 // acc (column 0 of an 8x8 accumulator, rows r0 + gid) += M[r0 .. r0+8, k0 .. k1) * v[k0 .. k1); M row-major, ld;
-// rows >= nrows contribute 0. k0, k1 multiples of 4.
-__device__ __forceinline__ double gemv8(const double* M, int ld, int r0, int nrows, int k0, int k1, const double* v,
-                                        int lane) {
+// rows >= nrows and columns >= kv contribute 0 (never read: the last row of a packed array ends at column kv).
+// k0, k1 multiples of 4.
+__device__ __forceinline__ double gemv8(const double* M, int ld, int r0, int nrows, int k0, int k1, int kv,
+                                        const double* v, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
   const bool rv = r0 + gid < nrows;
   const double* Mr = M + (int64_t)(rv ? r0 + gid : 0) * ld + tig;
@@ -30,15 +31,15 @@ __device__ __forceinline__ double gemv8(const double* M, int ld, int r0, int nro
   int k = k0;
 #pragma unroll 4
   for (; k + 8 <= k1; k += 8) {
-    const double a0 = rv ? __ldg(Mr + k) : 0.0;
-    const double a1 = rv ? __ldg(Mr + k + 4) : 0.0;
+    const double a0 = (rv && k + tig < kv) ? __ldg(Mr + k) : 0.0;
+    const double a1 = (rv && k + 4 + tig < kv) ? __ldg(Mr + k + 4) : 0.0;
     const double b0 = gid == 0 ? v[k + tig] : 0.0;
     const double b1 = gid == 0 ? v[k + 4 + tig] : 0.0;
     dmma(acc0, a0, b0);
     dmma(acc1, a1, b1);
   }
   if (k < k1) {
-    const double a0 = rv ? __ldg(Mr + k) : 0.0;
+    const double a0 = (rv && k + tig < kv) ? __ldg(Mr + k) : 0.0;
     const double b0 = gid == 0 ? v[k + tig] : 0.0;
     dmma(acc0, a0, b0);
   }
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs 
     const int32_t* perm = reinterpret_cast<const int32_t*>(LU + (int64_t)ne * ne);
     // t = r_e - B_e lambda_e (8-row tiles)
     for (int T = 0; T < nt; ++T) {
-      const double s = gemv8(Bm, nf, 8 * T, ne, 0, (nf + 3) & ~3, lam, lane);
+      const double s = gemv8(Bm, nf, 8 * T, ne, 0, (nf + 3) & ~3, nf, lam, lane);
       const int r = 8 * T + lane;
       if (lane < 8 && r < ne) t[r] = __ldg(re + r) - s;
     }
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs 
     for (int T = 0; T < nt; ++T) {
       const int r0 = 8 * T;
       if (T + 1 < nt) prefetch_tile(LU, ne, r0 + 8, ne, 0, r0 + 16, lane);
-      const double s = T > 0 ? gemv8(LU, ne, r0, ne, 0, r0, y, lane) : 0.0;
+      const double s = T > 0 ? gemv8(LU, ne, r0, ne, 0, r0, ne, y, lane) : 0.0;
       const int i = lane & 7, r = r0 + i;
       double Lr[8];
 #pragma unroll
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs 
     for (int T = nt - 1; T >= 0; --T) {
       const int r0 = 8 * T, rend = min(r0 + 8, ne);
       if (T > 0) prefetch_tile(LU, ne, r0 - 8, ne, r0 - 8, ne, lane);
-      const double s = rend < ne ? gemv8(LU, ne, r0, ne, rend, ne, y, lane) : 0.0;
+      const double s = rend < ne ? gemv8(LU, ne, r0, ne, rend, ne, ne, y, lane) : 0.0;
       const int i = lane & 7, r = r0 + i;
       double Ur[8];
 #pragma unroll

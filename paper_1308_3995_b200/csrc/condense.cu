@@ -145,7 +145,7 @@ __device__ __forceinline__ bool diag_factor(double* T, int ldT, int jb, int nb, 
 #pragma unroll
     for (int j = c; j < NB; ++j) prow[j] = __shfl_sync(0xffffffffu, d[j], c);
     const double pv = prow[c];
-    viol |= pv == 0.0;
+    viol |= !(fabs(pv) >= 2.2250738585072014e-308) || !(fabs(pv) < 1.0e300);   // zero/subnormal/huge/NaN: exact path (R7, R16)
     const double rp = fast_rcp(pv);
     if (lane == 0) rcs[c] = rp;
     if (lane > c && lane < NB) {
@@ -355,7 +355,7 @@ __device__ __forceinline__ void panel_factor_pivot(double* T, int ldT, int jb, i
     const double rp = 1.0 / pv;
     if (lane == 0) {
       piv[k] = pr;
-      if (pv == 0.0 && *flag == 0) *flag = k + 1;
+      if ((pv == 0.0 || pv != pv) && *flag == 0) *flag = k + 1;   // zero or NaN pivot (DESIGN R7)
     }
     for (int r = k + 1 + lane; r < ne; r += 32) {
       const double l = T[r * ldT + k] * rp;
@@ -742,6 +742,7 @@ cudaError_t launch_t(const CondenseArgs& a, int sms, cudaStream_t s) {
   int64_t grid = (int64_t)sms * per_sm;
   if (!T_SMEM) grid = sms;   // one scratch slab per resident CTA
   if (grid > a.count) grid = a.count;
+  grid = grid_cap(grid);
   kern<<<(unsigned)grid, THREADS, (size_t)smem, s>>>(a);
   return cudaGetLastError();
 }

@@ -497,7 +497,8 @@ __device__ void sweep_pivot(double* T, double* Cr, const SweepGeo& G, const doub
       if (lane == 0) {
         const int pr = bi < ne ? bi : k;
         piv[k] = pr;
-        if (!(T[(size_t)pr * ldT + k] != 0.0)) *shared_fail = k + 1;   // zero (or NaN) pivot
+        const double pv = T[(size_t)pr * ldT + k];
+        if (pv == 0.0 || pv != pv) *shared_fail = k + 1;   // zero or NaN pivot (DESIGN R7)
       }
     }
     __syncthreads();
@@ -987,6 +988,7 @@ cudaError_t launch_sweep_t(const CondenseArgs& a, int sms, cudaStream_t s) {
     grid = lb ? std::min<int64_t>(sms, std::max<int64_t>(1, atoll(lb) * 1024 * 1024 / slab)) : sms;
   }
   if (grid > a.count) grid = a.count;
+  grid = grid_cap(grid);
   kern<<<(unsigned)grid, NWARPS * 32, (size_t)smem, s>>>(a);
   return cudaGetLastError();
 }

@@ -211,6 +211,7 @@ cudaError_t launch_w(const CondenseArgs& a, int sms, cudaStream_t s) {
   int64_t grid = (int64_t)sms * per_sm;
   const int64_t need = (a.count + kWarpsPerCta - 1) / kWarpsPerCta;
   if (grid > need) grid = need;
+  grid = grid_cap(grid);
   warp_kernel<NE><<<(unsigned)grid, kWarpsPerCta * 32, smem, s>>>(a);
   return cudaGetLastError();
 }

@@ -19,6 +19,10 @@ constexpr int kMaxCT = (kMaxNf + 1 + 7) / 8;   // column tiles of [S | g] in pha
 
 __host__ __device__ constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// HDG_MAX_GRID (tests/tools only): caps the persistent grids of the condensation kernels, so a small mesh runs
+// several elements per CTA (the pipelined paths) — e.g. under compute-sanitizer. Unset: no cap.
+int64_t grid_cap(int64_t grid);
+
 // Geometry of the per-element working matrix T = [A | 0 | B | r_e | 0] (rows padded with zeros to R8, a
 // multiple of 16). Columns: A at [0, ne), B at CB = round_up(ne, 16), r_e at CB+nf, zero padding up to C8;
 // row stride ldT = 4 mod 16 doubles so that DMMA A-, B- and C-fragment accesses are bank-conflict free.
@@ -152,6 +156,8 @@ struct Plan {
   Skeleton sk;
   double* d_scratch = nullptr;
   int64_t scratch_doubles = 0;
+  double* d_send = nullptr;   // exchange buffers owned by the plan when the context has an NCCL communicator
+  double* d_recv = nullptr;
   int max_ne = 0, max_nf = 0;
   int64_t n_trace = 0;
 };
@@ -168,6 +174,7 @@ struct hdg_ctx_s {
   hdg::Plan plan;
   int64_t launches = 0;
   long long* trace = nullptr;
+  void* nccl_comm = nullptr;   // ncclComm_t (nranks > 1 with an NCCL id): a7 runs inside hdg_assemble_*
 };
 
 // kernel launchers (defined in the .cu files); return cudaError_t of the launch
@@ -187,4 +194,11 @@ cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, dou
 cudaError_t launch_accumulate(const Plan& p, const double* recv, double* K, double* E, cudaStream_t s,
                               int64_t* launches);
 cudaError_t launch_first_error(const int32_t* info, int64_t n, int64_t* d_out, cudaStream_t s);
+// comm.cu (NCCL resolved at run time)
+bool nccl_available(std::string* err);
+bool nccl_unique_id(unsigned char* out, std::string* err);
+bool nccl_comm_init(void** comm, int nranks, int rank, const unsigned char* id, std::string* err);
+void nccl_comm_destroy(void* comm);
+bool nccl_exchange(void* comm, const Plan& p, int rank, int nranks, const double* send, double* recv, cudaStream_t s,
+                   std::string* err);
 }  // namespace hdg

@@ -254,31 +254,36 @@ cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s) {
   Skeleton& k = p.sk;
   const int64_t nrows = k.f1 - k.f0;
   int64_t *cnt = nullptr, *vals = nullptr, *rs = nullptr, *vs = nullptr;
+  // every allocation is checked (OOM -> the caller's HDG_ERR_NOMEM, no launch through a null pointer); the
+  // temporaries are freed on every exit path, the CSR arrays by free_plan
+  auto done = [&](cudaError_t e) {
+    cudaFree(cnt); cudaFree(vals); cudaFree(rs); cudaFree(vs);
+    return e;
+  };
   cudaError_t e;
-  if ((e = cudaMalloc(&cnt, sizeof(int64_t) * (nrows + 1))) != cudaSuccess) return e;
-  cudaMalloc(&vals, sizeof(int64_t) * (nrows + 1));
-  cudaMalloc(&rs, sizeof(int64_t) * (nrows + 1));
-  cudaMalloc(&vs, sizeof(int64_t) * (nrows + 1));
+  if ((e = cudaMalloc(&cnt, sizeof(int64_t) * (nrows + 1))) != cudaSuccess) return done(e);
+  if ((e = cudaMalloc(&vals, sizeof(int64_t) * (nrows + 1))) != cudaSuccess) return done(e);
+  if ((e = cudaMalloc(&rs, sizeof(int64_t) * (nrows + 1))) != cudaSuccess) return done(e);
+  if ((e = cudaMalloc(&vs, sizeof(int64_t) * (nrows + 1))) != cudaSuccess) return done(e);
   if (nrows > 0)
     sym_count_kernel<<<blocks_for(nrows), 256, 0, s>>>(p.d_elem_face, p.d_face_elem, p.d_face_ndof, k.f0, nrows, cnt, vals);
   scan_kernel<<<1, 1024, 0, s>>>(cnt, nrows, rs);
   scan_kernel<<<1, 1024, 0, s>>>(vals, nrows, vs);
   int64_t tot[2];
-  cudaMemcpyAsync(&tot[0], rs + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(&tot[1], vs + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(&tot[0], rs + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return done(e);
+  if ((e = cudaMemcpyAsync(&tot[1], vs + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return done(e);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return done(e);
   k.nnzb = tot[0];
   k.nvals = tot[1];
-  cudaMalloc(&k.d_row_ptr, sizeof(int32_t) * (nrows + 1));
-  cudaMalloc(&k.d_col_idx, sizeof(int32_t) * (k.nnzb > 0 ? k.nnzb : 1));
-  cudaMalloc(&k.d_blk_off, sizeof(int64_t) * (k.nnzb + 1));
-  cudaMalloc(&k.d_blk_row, sizeof(int32_t) * (k.nnzb > 0 ? k.nnzb : 1));
+  if ((e = cudaMalloc(&k.d_row_ptr, sizeof(int32_t) * (nrows + 1))) != cudaSuccess) return done(e);
+  if ((e = cudaMalloc(&k.d_col_idx, sizeof(int32_t) * (k.nnzb > 0 ? k.nnzb : 1))) != cudaSuccess) return done(e);
+  if ((e = cudaMalloc(&k.d_blk_off, sizeof(int64_t) * (k.nnzb + 1))) != cudaSuccess) return done(e);
+  if ((e = cudaMalloc(&k.d_blk_row, sizeof(int32_t) * (k.nnzb > 0 ? k.nnzb : 1))) != cudaSuccess) return done(e);
   sym_fill_kernel<<<blocks_for(nrows + 1), 256, 0, s>>>(p.d_elem_face, p.d_face_elem, p.d_face_ndof, k.f0, nrows, rs, vs,
                                                         k.d_row_ptr, k.d_col_idx, k.d_blk_off, k.d_blk_row);
   e = cudaStreamSynchronize(s);
-  cudaFree(cnt); cudaFree(vals); cudaFree(rs); cudaFree(vs);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return done(e);
 }
 
 cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, double* K, double* E, double* send,

@@ -281,3 +281,63 @@ def test_sweep_hp_buckets(cuda, monkeypatch):
     """configs[4] with the sweep kernel forced: its supported (n_e, n_f) buckets next to panel-kernel buckets."""
     monkeypatch.setenv("HDG_CONDENSE_KERNEL", "sweep")
     check_all(gen.config("C5", nr=5, nt=10))
+
+
+@pytest.mark.parametrize("name,nr,nt,P", [("C2", 4, 10, 2), ("C5", 4, 12, 3), ("C3", 3, 8, 4)])
+def test_exchange_kernels_on_oracle_S_bitwise(cuda, name, nr, nt, P):
+    """a6/a7 anchored to the oracle: the ORACLE's S and g, split into P element slabs, go through libhdg's own
+    pack_kernel (inside hdg_assemble_skeleton) -> device buffer swap (the transport, done here by copies on one
+    GPU) -> accumulate_kernel; the concatenated owned rows equal oracle.assemble of the whole mesh bit for bit
+    (P12; left contribution first, then right)."""
+    import torch
+    import paper_1308_3995_b200 as hdg
+    w = gen.config(name, nr=nr, nt=nt)
+    ref = oracle.pipeline(w, lam=np.zeros(w.n_trace))
+    c = ref["cond"]
+    reb = np.array([(r * w.E) // P for r in range(P + 1)], dtype=np.int64)
+    reb[1] -= 3                                   # uneven slabs
+    ranks = []
+    for r in range(P):
+        eb, n = int(reb[r]), int(reb[r + 1] - reb[r])
+        ctx = hdg.Context(0, r, P)
+        info = ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne, eb, n, reb)
+        S = to_dev(c["S"][c["off_S"][eb]:c["off_S"][eb + n]])
+        g = to_dev(c["g"][c["off_g"][eb]:c["off_g"][eb + n]])
+        K, E = ctx.alloc("K"), ctx.alloc("E")
+        send = ctx.alloc("send") if info.send_doubles > 0 else None
+        ctx.assemble_skeleton(S, g, K, E, send=send)
+        ranks.append(dict(ctx=ctx, info=info, K=K, E=E, send=send, counts=ctx.exchange_counts()))
+    for r in range(P):
+        me = ranks[r]
+        sc, sd, rc, rd = me["counts"]
+        recv = me["ctx"].alloc("recv")
+        for q in range(P):
+            if q == r or rc[q] == 0:
+                continue
+            osc, osd, _, _ = ranks[q]["counts"]
+            assert osc[r] == rc[q]
+            recv[rd[q]:rd[q] + rc[q]] = ranks[q]["send"][osd[r]:osd[r] + osc[r]]
+        me["ctx"].skeleton_accumulate(recv, me["K"], me["E"])
+    torch.cuda.synchronize()
+    K = np.concatenate([x["K"].cpu().numpy()[:x["info"].nvals] for x in ranks])
+    E = np.concatenate([x["E"].cpu().numpy()[:x["info"].n_owned_trace] for x in ranks])
+    assert np.array_equal(K, ref["K"])
+    assert np.array_equal(E, ref["E"])
+
+
+def test_nccl_context_bootstrap_single_rank(cuda):
+    """The in-library NCCL bootstrap on one GPU: hdg_get_unique_id -> hdg_ctx_create with the id (a one-rank
+    communicator); the context reports its communicator and the whole path still matches the oracle."""
+    import paper_1308_3995_b200 as hdg
+    nid = hdg.get_unique_id()
+    assert len(nid) == 128
+    ctx = hdg.Context(0, 0, 1, nccl_id=nid)
+    assert ctx.has_comm
+    w = gen.config("C2", nr=3, nt=6)
+    blk = gen.host_blocks(w)
+    lam = gen.host_lambda(w)
+    ref = oracle.pipeline(w, blk=blk, lam=lam)
+    r = run_gpu(w, blk=blk, lam=lam, ctx=ctx)
+    assert np.array_equal(r["col_idx"].cpu().numpy()[:r["info"].nnzb], ref["sym"][1])
+    assert rel_per_block(r["K"].cpu().numpy(), ref["K"], ref["sym"][2]) < KTOL
+    ctx.close()
