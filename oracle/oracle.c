@@ -78,8 +78,13 @@ int oracle_condense_one(int ne, int nf, const double* A, const double* B, const 
   memcpy(LU, A, sizeof(double) * (size_t)ne * ne);
   const int info = oracle_lu(ne, LU, piv);
   if (info) {
+    /* S7 / DESIGN.md R7: a singular element has no Schur complement and no reconstruction. Its S, g are NaN, and
+     * its saved factors are NaN with the unreached interchanges set to none, so O6 returns NaN for u (instead of
+     * reading pivots the factorization never wrote). */
     for (int64_t i = 0; i < (int64_t)nf * nf; ++i) S[i] = NAN;
     for (int i = 0; i < nf; ++i) g[i] = NAN;
+    for (int k = info - 1; k < ne; ++k) piv[k] = k;
+    for (int64_t i = 0; i < (int64_t)ne * ne; ++i) LU[i] = NAN;
     return info;
   }
   const int w = nf + 1;                                /* X = A^-1 [B | r_e] */

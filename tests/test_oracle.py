@@ -271,6 +271,25 @@ def test_singular_element_info():
     assert np.isnan(S).all() and np.isnan(g).all()
 
 
+def test_singular_element_in_mesh_pipeline():
+    """A singular element inside a mesh: info = k+1 for it alone (a zero column stays exactly zero under the
+    elimination of the columns before it), its S, g and u are NaN (no reconstruction of a singular local block),
+    every other element's u is finite and still satisfies its local residual (P6)."""
+    import gen
+    w = gen.make_workload("C3", nr=2, nt=3, m_elem=4, p_fixed=4, seed=gen.SEED_BASE + 3)
+    blk = gen.host_blocks(w)
+    bad, col = 4, 23
+    A = blk["A"][blk["off_A"][bad]:blk["off_A"][bad + 1]].reshape(60, 60)
+    A[:, col] = 0.0
+    lam = gen.host_lambda(w)
+    ref = oracle.pipeline(w, blk=blk, lam=lam)
+    info = ref["cond"]["info"]
+    assert info[bad] == col + 1 and (np.delete(info, bad) == 0).all()
+    ou = ref["off_u"]
+    assert np.isnan(ref["u"][ou[bad]:ou[bad + 1]]).all()
+    assert np.isfinite(np.delete(ref["u"], np.arange(ou[bad], ou[bad + 1]))).all()
+
+
 # ------------------------------------------------------------------------------------------------------------
 # P10: counts and the worked example
 def test_p10_worked_example():
