@@ -137,7 +137,7 @@ __device__ __forceinline__ void solve_transposed(const double* LU, const int32_t
     if (lane < 8 && r < ne) vec[r] = yi;
     __syncwarp();
   }
-  for (int k = lane; k < ne; k += 32) out[__ldg(perm + k)] = vec[k];
+  for (int k = lane; k < ne; k += 32) out[min((unsigned)__ldg(perm + k), (unsigned)ne - 1)] = vec[k];
   __syncwarp();
 }
 

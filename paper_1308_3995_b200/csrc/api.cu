@@ -63,6 +63,7 @@ void free_plan(Plan& p) {
   cudaFree(p.sk.d_send_items); cudaFree(p.sk.d_recv_items);
   cudaFree(p.d_scratch);
   cudaFree(p.d_send); cudaFree(p.d_recv);
+  cudaFree(p.d_redo); cudaFree(p.d_redo_count); cudaFree(p.d_mark);
   p = Plan();
 }
 
@@ -342,10 +343,13 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     B.warp = warp_supported(B.ne, B.nf) && fk != "sweep" && fk != "panel";
     B.sweep = !B.warp && sweep_supported(B.ne, B.nf, ctx->smem_optin) && fk != "panel" &&
               (B.ne >= 96 || B.ne <= 32 || fk == "sweep");
+    // the row-tile kernel (condense_rows.cu): HDG_CONDENSE_KERNEL=rows
+    B.rows = !B.warp && fk == "rows" && rows_supported(B.ne, B.nf, ctx->smem_optin);
+    if (B.rows) B.sweep = false;
     // elements larger than one SM (C5's n_e = 180, 252): the sweep kernel on an L2-resident global slab
-    B.sweep_gt = !B.warp && !B.sweep && !B.t_in_smem && fk != "panel" && sweep_gt_supported(B.ne, B.nf);
-    if (!B.warp && !B.sweep && !B.sweep_gt && !B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
-    if (B.sweep || B.sweep_gt) {   // exact-path (and GT working) slab per resident CTA (at most 2 per SM)
+    B.sweep_gt = !B.warp && !B.sweep && !B.rows && !B.t_in_smem && fk != "panel" && sweep_gt_supported(B.ne, B.nf);
+    if (!B.warp && !B.sweep && !B.sweep_gt && !B.rows && !B.t_in_smem) scratch = std::max(scratch, geo.t_doubles() * ctx->sms);
+    if (B.sweep || B.sweep_gt || B.rows) {   // exact-path (and GT working) slab per resident CTA (at most 2 per SM)
       const SweepGeo sg(B.ne, B.nf);
       scratch = std::max(scratch, ((int64_t)sg.RA * sg.ldT + (int64_t)sg.NF8 * sg.ldC) * 2 * ctx->sms);
     }
@@ -356,6 +360,13 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     if (cudaMalloc(&p.d_scratch, sizeof(double) * scratch) != cudaSuccess)
       return fail(ctx, HDG_ERR_NOMEM, "hdg_plan: scratch of %lld doubles", (long long)scratch);
     p.scratch_doubles = scratch;
+  }
+  if (std::any_of(p.buckets.begin(), p.buckets.end(), [](const Bucket& b) { return b.rows; })) {
+    if (cudaMalloc(&p.d_redo, sizeof(int32_t) * std::max<int64_t>(1, n)) != cudaSuccess ||
+        cudaMalloc(&p.d_redo_count, sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&p.d_mark, sizeof(int32_t) * std::max<int64_t>(1, n)) != cudaSuccess)
+      return fail(ctx, HDG_ERR_NOMEM, "hdg_plan: redo list");
+    HDG_CUDA(ctx, cudaMemset(p.d_mark, 0, sizeof(int32_t) * std::max<int64_t>(1, n)));
   }
 
   // ---- owned skeleton rows ---------------------------------------------------------------------------------------
@@ -450,7 +461,9 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
     a.scratch = p.d_scratch;
     a.trace = ctx->trace;
     a.debug = getenv("HDG_DEBUG_MODE") ? atoi(getenv("HDG_DEBUG_MODE")) : 0;
+    a.redo = p.d_redo; a.redo_count = p.d_redo_count; a.mark = p.d_mark;
     if (b.warp) HDG_CUDA(ctx, launch_condense_warp(a, ctx->sms, s, &ctx->launches));
+    else if (b.rows) HDG_CUDA(ctx, launch_condense_rows(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
     else if (b.sweep) HDG_CUDA(ctx, launch_condense_sweep(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
     else if (b.sweep_gt) HDG_CUDA(ctx, launch_condense_sweep_gt(a, ctx->sms, s, &ctx->launches));
     else HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));

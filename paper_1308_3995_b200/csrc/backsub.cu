@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs 
     }
     __syncwarp();
     // apply P: row i of P t is t[perm[i]]
-    for (int i = lane; i < ne; i += 32) y[i] = t[__ldg(perm + i)];
+    for (int i = lane; i < ne; i += 32) y[i] = t[min((unsigned)__ldg(perm + i), (unsigned)ne - 1)];
     __syncwarp();
     // forward: L y = P t (unit lower)
     for (int T = 0; T < nt; ++T) {
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) backsub_rows_kernel(const
 #pragma unroll
     for (int s = 0; s < MAXR; ++s) {
       const int i = lane + 32 * s;
-      if (i < ne) t[s] = x_s[w][__ldg(perm + i)];
+      if (i < ne) t[s] = x_s[w][min((unsigned)__ldg(perm + i), (unsigned)ne - 1)];
     }
     // reciprocals of U's diagonal for the rows this lane owns (off the dependency chain)
     double rd[MAXR];

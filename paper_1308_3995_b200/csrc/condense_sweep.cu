@@ -993,7 +993,34 @@ cudaError_t launch_sweep_t(const CondenseArgs& a, int sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// The exact path over a device-side list of elements (the row-tile kernel's failed speculations): one element
+// per CTA at a time in the CTA's global scratch slab; the list length is read on the device (0: immediate exit).
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) exact_list_kernel(const CondenseArgs a, const int32_t* list,
+                                                             const int32_t* count) {
+  extern __shared__ __align__(16) int ish[];
+  const SweepGeo G(a.ne, a.nf);
+  int* piv = ish;
+  int* sfail = ish + G.RA;
+  double* X = a.scratch + (size_t)blockIdx.x * (size_t)(G.RA * G.ldT + G.NF8 * G.ldC);
+  const int n = *count;
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    const int64_t l = list[q];
+    exact_element<THREADS>(a.A + a.offA[l], a.B + a.offB[l], a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l],
+                           a.rf + a.offRf[l], a.S + a.offS[l], a.g + a.offG[l],
+                           reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, a.ne, a.nf, X, piv, sfail,
+                           threadIdx.x);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_exact_list(const CondenseArgs& a, const int32_t* list, const int32_t* count, int grid, cudaStream_t s) {
+  const SweepGeo G(a.ne, a.nf);
+  const size_t smem = sizeof(int) * (G.RA + 4);
+  exact_list_kernel<256><<<(unsigned)std::max(1, grid), 256, smem, s>>>(a, list, count);
+  return cudaGetLastError();
+}
 
 // Whether the sweep kernel with T in shared memory handles (ne, nf).
 bool sweep_supported(int ne, int nf, size_t smem_optin) {

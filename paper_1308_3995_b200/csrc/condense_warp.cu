@@ -115,8 +115,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
       }
       __syncwarp();
     }
+    // ---- factors: L\U rows in GEPP order (row-major, coalesced per row) + the permutation — also for a singular
+    //      element (its partial factors; prow is a permutation however far the elimination got), so the factor
+    //      record always holds a valid permutation for the solve kernels ---------------------------------------------
     double* LU = reinterpret_cast<double*>(a.factors + a.offF[l]);
     int32_t* perm = reinterpret_cast<int32_t*>(LU + (int64_t)ne * ne);
+    for (int i = 0; i < ne; ++i)
+      if (c0 < ne) LU[(int64_t)i * ne + c0] = T[i * kLdT + c0];
+    if (lane < ne) perm[lane] = prow;
     if (lane == 0) a.info[l] = fail;
     if (fail) {
       double* S = a.S + a.offS[l];
@@ -126,10 +132,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
       __syncwarp();
       continue;
     }
-    // ---- factors: L\U rows in GEPP order (row-major, coalesced per row) + the permutation ---------------------------
-    for (int i = 0; i < ne; ++i)
-      if (c0 < ne) LU[(int64_t)i * ne + c0] = T[i * kLdT + c0];
-    if (lane < ne) perm[lane] = prow;
     // ---- X = U^-1 W: each lane its columns of W ---------------------------------------------------------------------
     {
       const bool a0 = c0 >= ne && c0 < nc, a1 = c1 < nc;

@@ -87,6 +87,9 @@ struct CondenseArgs {
   double* scratch;        // global workspace for T when it does not fit in shared memory
   long long* trace;       // instrumentation: clock64 stamps of CTA 0 (NULL = off)
   int debug;              // profiling experiments only (HDG_DEBUG_MODE): 1 = workers skip their MMA work
+  int32_t* redo;          // row-tile kernel: elements whose GEPP speculation failed (redone on the exact path)
+  int32_t* redo_count;
+  int32_t* mark;          // [n] per-element failed-speculation marks (zero between calls)
 };
 
 struct BacksubArgs {
@@ -125,6 +128,7 @@ struct Bucket {
   bool sweep;         // condensed by the sweep kernel (condense_sweep.cu)
   bool warp;          // condensed by the warp-per-element kernel (condense_warp.cu)
   bool sweep_gt;      // condensed by the sweep kernel with its working matrix in global scratch
+  bool rows;          // condensed by the row-tile kernel (condense_rows.cu)
 };
 
 // Skeleton assembly data (owned rows).
@@ -156,6 +160,9 @@ struct Plan {
   Skeleton sk;
   double* d_scratch = nullptr;
   int64_t scratch_doubles = 0;
+  int32_t* d_redo = nullptr;       // [n] + count: the row-tile kernel's redo list, and its per-element marks
+  int32_t* d_redo_count = nullptr;
+  int32_t* d_mark = nullptr;
   double* d_send = nullptr;   // exchange buffers owned by the plan when the context has an NCCL communicator
   double* d_recv = nullptr;
   int max_ne = 0, max_nf = 0;
@@ -186,6 +193,10 @@ bool sweep_gt_supported(int ne, int nf);
 cudaError_t launch_condense_sweep_gt(const CondenseArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_condense_warp(const CondenseArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_condense_sweep(const CondenseArgs& a, int sms, size_t smem_optin, cudaStream_t s, int64_t* launches);
+bool rows_supported(int ne, int nf, size_t smem_optin);
+cudaError_t launch_condense_rows(const CondenseArgs& a, int sms, size_t smem_optin, cudaStream_t s, int64_t* launches);
+// exact path (unblocked GEPP with the warp pivot search) for the listed elements (count on the device)
+cudaError_t launch_exact_list(const CondenseArgs& a, const int32_t* list, const int32_t* count, int grid, cudaStream_t s);
 cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_adjoint(const AdjointArgs& a, int mode, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s);
