@@ -330,6 +330,174 @@ def setup_workload(config: str, rank: int = 0, world: int = 1, local: int = 0, s
     return out
 
 
+def run_chunked(args, rank, world, local, dmma_peak):
+    """C5 (configs[4], ~490 GB) on N GPUs, whole mesh: the mesh is cut into V = max(8, N) element slabs ("virtual
+    ranks"); rank r processes its V/N slabs one after another, each slab's inputs generated in HBM
+    (outside the timed region: "C5 at P = 1, 2: sum of per-chunk kernel times; generation and H2D
+    excluded"), condensed, assembled (its K rows stay resident) and back-substituted. The shared-face exchange
+    between slabs follows once per step: slabs on the same GPU by device copies, slabs on other GPUs through
+    torch.distributed point-to-point (NCCL); then every slab's ordered accumulate. Step time = the sum of the
+    slabs' condense + assemble + back-substitute times + the exchange/accumulate time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import gen
+    import paper_1308_3995_b200 as hdg
+    dev = torch.device("cuda", local)
+    w = gen.config(args.config)
+    V = max(8, world)
+    if V % world:
+        raise SystemExit(f"--gpus {world}: the {V} C5 slabs must divide evenly over the ranks")
+    vb = slab_bounds(w.E, V)
+    mine = list(range(rank * V // world, (rank + 1) * V // world))
+    owner = lambda v: v * world // V                                     # noqa: E731
+    stream = torch.cuda.Stream(dev)
+    sl = {}
+    for v in mine:
+        eb, n = int(vb[v]), int(vb[v + 1] - vb[v])
+        ctx = hdg.Context(local, v, V)
+        info = ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne, eb, n, vb)
+        sl[v] = dict(ctx=ctx, info=info, eb=eb, n=n, K=ctx.alloc("K"), E=ctx.alloc("E"), send=ctx.alloc("send"),
+                     recv=ctx.alloc("recv"), counts=ctx.exchange_counts())
+    # per-slab work buffers, sized for the largest owned slab, reused slab after slab
+    keys = ("A", "B", "C", "D", "re", "rf")
+    big = {k: max(int(w.off[k][sl[v]["eb"] + sl[v]["n"]] - w.off[k][sl[v]["eb"]]) for v in mine) for k in keys}
+    inp = {k: torch.empty(max(big[k], 2), dtype=torch.float64, device=dev) for k in keys}
+    outs = {k: max(getattr(sl[v]["info"], f) for v in mine) for k, f in (("S", "len_S"), ("g", "len_g"),
+                                                                          ("u", "len_u"), ("F", "factor_bytes"))}
+    S = torch.empty(outs["S"], dtype=torch.float64, device=dev)
+    g = torch.empty(outs["g"], dtype=torch.float64, device=dev)
+    u = torch.empty(outs["u"], dtype=torch.float64, device=dev)
+    F = torch.empty(outs["F"], dtype=torch.uint8, device=dev)
+    infot = torch.empty(max(sl[v]["n"] for v in mine), dtype=torch.int32, device=dev)
+    lam = torch.empty(w.n_trace, dtype=torch.float64, device=dev)
+    with torch.cuda.stream(stream):
+        gen.device_lambda(w, lam, torch.from_numpy(w.face_ndof).to(dev), torch.from_numpy(w.face_off).to(dev))
+    dne = {v: torch.from_numpy(w.elem_ne[sl[v]["eb"]:sl[v]["eb"] + sl[v]["n"]].copy()).to(dev) for v in mine}
+    dnf = {v: torch.from_numpy(w.elem_nf[sl[v]["eb"]:sl[v]["eb"] + sl[v]["n"]].copy()).to(dev) for v in mine}
+    doff = {(v, k): torch.from_numpy(w.off[k][sl[v]["eb"]:sl[v]["eb"] + sl[v]["n"] + 1] - w.off[k][sl[v]["eb"]]).to(dev)
+            for v in mine for k in keys}
+    torch.cuda.synchronize()
+    launches = [0]
+
+    def step(timed):
+        evs = []
+        for v in mine:
+            x = sl[v]
+            with torch.cuda.stream(stream):      # generation of this slab's inputs: outside the timed region
+                for k in keys:
+                    gen.device_blocks(w, k, inp[k], e0=x["eb"], n=x["n"], off=doff[(v, k)], stream=stream.cuda_stream,
+                                      dev_ne=dne[v], dev_nf=dnf[v])
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ctx = x["ctx"]
+            e[0].record(stream)
+            ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], S, g, F, infot, stream=stream)
+            launches[0] += ctx.launch_count()
+            e[1].record(stream)
+            ctx.assemble_skeleton(S, g, x["K"], x["E"], send=x["send"], stream=stream)
+            launches[0] += ctx.launch_count()
+            e[2].record(stream)
+            ctx.backsubstitute(F, inp["B"], inp["re"], lam, u, stream=stream)
+            launches[0] += ctx.launch_count()
+            e[3].record(stream)
+            evs.append(e)
+        # a7 between slabs: same-GPU peers by copies, other GPUs by NCCL point-to-point (one canonical order of
+        # (source slab, destination slab) pairs on every rank, so the messages between two ranks match)
+        ex = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ex[0].record(stream)
+        with torch.cuda.stream(stream):
+            ops = []
+            for src in range(V):
+                for dst in range(V):
+                    if src == dst:
+                        continue
+                    so, do = owner(src), owner(dst)
+                    if so != rank and do != rank:
+                        continue
+                    if so == rank:
+                        sc, sd, _, _ = sl[src]["counts"]
+                        cnt, off = int(sc[dst]), int(sd[dst])
+                    else:
+                        _, _, rc, rd = sl[dst]["counts"]
+                        cnt, off = int(rc[src]), int(rd[src])
+                    if cnt == 0:
+                        continue
+                    if so == rank and do == rank:
+                        _, _, rc, rd = sl[dst]["counts"]
+                        sl[dst]["recv"][int(rd[src]):int(rd[src]) + cnt].copy_(sl[src]["send"][off:off + cnt])
+                    elif so == rank:
+                        ops.append(dist.P2POp(dist.isend, sl[src]["send"][off:off + cnt], do))
+                    else:
+                        ops.append(dist.P2POp(dist.irecv, sl[dst]["recv"][off:off + cnt], so))
+            if ops:
+                for wk in dist.batch_isend_irecv(ops):
+                    wk.wait()
+            for v in mine:
+                sl[v]["ctx"].skeleton_accumulate(sl[v]["recv"], sl[v]["K"], sl[v]["E"], stream=stream)
+                launches[0] += sl[v]["ctx"].launch_count()
+        ex[1].record(stream)
+        torch.cuda.synchronize()
+        if not timed:
+            return None
+        cond = sum(e[0].elapsed_time(e[1]) for e in evs)
+        asm = sum(e[1].elapsed_time(e[2]) for e in evs)
+        bs = sum(e[2].elapsed_time(e[3]) for e in evs)
+        xch = ex[0].elapsed_time(ex[1])
+        return cond, asm, bs, xch
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        step(False)
+    for v in mine:
+        bad, code = sl[v]["ctx"].first_error(infot[:sl[v]["n"]], stream=stream)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark()
+    launches[0] = 0
+    res = [step(True) for _ in range(args.steps)]
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([sum(r[i] for r in res) / args.steps for i in range(4)], dtype=torch.float64, device=dev)
+    t_step = torch.tensor([sum(res[-1])], dtype=torch.float64, device=dev)
+    tot = torch.tensor([sum(sum(r) for r in res) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    cond_ms, asm_ms, bs_ms, x_ms = t.tolist()
+    ms_step = tot.item()
+    if rank == 0:
+        ne = w.elem_ne[int(vb[mine[0]]):int(vb[mine[-1] + 1])]
+        nf = w.elem_nf[int(vb[mine[0]]):int(vb[mine[-1] + 1])]
+        work = algorithmic(ne, nf)
+        fp64_peak = dmma_peak or 37.2
+        ach = work["condense_flops"] / (cond_ms * 1e-3) / 1e12
+        line = {"metric": METRIC, "value": w.E / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded Philox blocks with BASELINE.json distributions, generated in HBM per slab)",
+                "config": {"workload": f"C5 whole mesh ({w.E} elements) in {V} slabs, {len(mine)} per GPU",
+                           "elements": w.E, "n_e": int(w.elem_ne.max()), "n_f": int(w.elem_nf.max()),
+                           "parallelism": f"element slabs x{world} (x{len(mine)} chunks per GPU)",
+                           "l2": "inputs exceed the 126 MB L2; no flush needed",
+                           "step": "per slab: condense + assemble_skeleton + backsubstitute; then the shared-face "
+                                   "exchange between slabs + ordered accumulate",
+                           "timing": "sum of the per-slab CUDA-event times + exchange; slab input generation "
+                                     "excluded (SURVEY.md §8(d))"},
+                "condense_ms": cond_ms, "assemble_ms": asm_ms, "backsub_ms": bs_ms, "exchange_ms": x_ms,
+                "condense_per_s": w.E / (cond_ms * 1e-3 * world / world), "backsub_per_s": w.E / (bs_ms * 1e-3),
+                "roofline": {"bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                             "frac": ach / fp64_peak, "traffic": None,
+                             "kernel": "hdg_condense over C5's hp buckets (sweep GT / sweep / panel / warp)",
+                             "flops_per_rank_step": work["condense_flops"]},
+                "gpu_launches": launches[0] // max(1, args.steps) * args.steps, "clocks": clk,
+                "cpu_baseline": None, "e2e": None}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+
 def run_step(wl, ev=None):
     """One step of the hot path on the workload; returns the libhdg launches issued."""
     import paper_1308_3995_b200 as hdg
@@ -373,8 +541,6 @@ def main():
     ap.add_argument("--slab", default=None,
                     help="r/P: time rank r's slab of a P-way partition on this one GPU (default for C5: 0/8)")
     args = ap.parse_args()
-    if args.slab is None and args.config == "C5" and int(os.environ.get("WORLD_SIZE", "1")) < 4:
-        args.slab = "0/8"      # C5 (~490 GB) does not fit one B200: one rank's share of the 8-GPU partition
     if args.slab is not None:
         r_, p_ = (int(x) for x in args.slab.split("/"))
         args.slab = (r_, p_)
@@ -396,6 +562,9 @@ def main():
     dev = torch.device("cuda", local)
     dmma_peak, dfma_peak = (fp64_peak_in_run() if rank == 0 else (None, None))
 
+    if args.config == "C5" and args.slab is None:
+        # C5 (~490 GB of inputs) does not fit one B200: the whole mesh in element slabs, several per GPU
+        return run_chunked(args, rank, world, local, dmma_peak)
     wl = setup_workload(args.config, rank, world, local, slab=args.slab)
     if args.path == "adjoint":
         return run_adjoint(args, wl, rank, world, local)
