@@ -319,3 +319,36 @@ def device_philox_raw(ctr, key):
     assert rc == 0
     torch.cuda.synchronize()
     return o.cpu().numpy().view(np.uint32).reshape(n, 4)
+
+
+# ------------------------------------------------------------------------------------------------------------
+# Pseudo-time relaxation inputs (§8(f) NEXT #4). These are INPUTS of the re-condensation (like
+# A_e), not the method's arithmetic: a CFL number per Newton step from the paper's ramp, and per element a
+# seeded stand-in for the spectral-radius estimate (lambda_c + 4 lambda_v) of the local time step
+# dt_K = CFL |K| / (lambda_c + 4 lambda_v).
+def cfl_ramp(n: int, n0: int = 10, c0: float = 10.0) -> float:
+    """CFL^n for n <= n0: c0 (3 (n/n0)^2 - 2 (n/n0)^3) (PAPER.md eq. cfl, the ramping phase)."""
+    x = min(max(n / n0, 0.0), 1.0)
+    return c0 * (3.0 * x * x - 2.0 * x * x * x)
+
+
+def pseudo_time_shift(w: Workload, cfl: float, e0: int = 0, n: int | None = None) -> np.ndarray:
+    """Per-element diagonal shift packed like r_e: |K| / dt_K = (lambda_c + 4 lambda_v)_K / CFL on the element's
+    w unknowns (an orthonormal modal basis: M_e = |K| I), 0 on the gradient unknowns q. Element unknowns are
+    [Q; W] basis-major (DESIGN R4): for NS mixed (m_elem = 12) W is the last 4 n(p) unknowns, for Euler all.
+    The spectral-radius stand-in is 1 + |z_K| with z_K ~ N(0, 1) from a seeded numpy generator (keyed by the
+    workload seed and the element id, so slabs agree)."""
+    if n is None:
+        n = w.E - e0
+    lam = np.empty(n)
+    for k in range(n):
+        rng = np.random.default_rng([w.seed, 9, e0 + k])
+        lam[k] = 1.0 + abs(rng.standard_normal())
+    out = np.zeros(int(w.off["re"][e0 + n] - w.off["re"][e0]))
+    o = 0
+    for k in range(n):
+        ne = int(w.elem_ne[e0 + k])
+        nw = 4 * (ne // w.m_elem) if w.m_elem != 4 else ne
+        out[o + ne - nw:o + ne] = lam[k] / cfl
+        o += ne
+    return out

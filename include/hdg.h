@@ -131,6 +131,18 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
                         const double* r_e, const double* r_f, double* S, double* g, void* factors,
                         int32_t* info, hdg_stream stream);
 
+/* Re-condensation with a diagonal shift (§8(f) NEXT #4): the pseudo-time relaxation adds <phi_h, dw_h / dt> to
+ * the linearised system (backward Euler in an artificial time, local time step dt_K per element),
+ * i.e. M_e / dt_K on the element's w unknowns. With an orthonormal (modal) basis M_e = |K| I, so the term is the
+ * diagonal shift |K| / dt_K = (lambda_c + 4 lambda_v) / CFL^n on those unknowns (0 on q). This call condenses
+ * A_e + diag(shift_e) exactly as hdg_condense condenses A_e — the shift is added while the kernels stage A_e (no
+ * extra pass over A in HBM), so every Newton step re-condenses the changed matrix at the cost of hdg_condense.
+ * shift: device, packed like r_e (n_e doubles per element, 16-byte aligned), read only. Everything else, including
+ * info and the saved factors (of the shifted matrix), as hdg_condense. */
+hdg_status hdg_condense_shifted(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                                const double* r_e, const double* r_f, const double* shift, double* S, double* g,
+                                void* factors, int32_t* info, hdg_stream stream);
+
 /* a6 (+a7 pack) assembly of the owned skeleton rows: K[f, f'] = sum over local elements e adjacent to both of
  * S_e[slot(f), slot(f')], E[f] = sum of g_e[slot(f)], contributions taken left (lower element id) then right
  * (SURVEY.md S10). Block-CSR over owned rows: row_ptr [n_owned_faces + 1] int32 (block
@@ -202,6 +214,17 @@ hdg_status hdg_assemble_adjoint(hdg_ctx ctx, const double* S, const double* gt, 
  * adjoint trace vector lambda_t [n_trace] in slot order. C: the packed input of hdg_condense. ut: packed like u. */
 hdg_status hdg_backsubstitute_adjoint(hdg_ctx ctx, const void* factors, const double* C, const double* rt_e,
                                       const double* lambda_t, double* ut, hdg_stream stream);
+
+/* DG-vs-HDG global-matrix size (§8(f) NEXT #4; "blocks ... O(m^2 p^2(d-1)) entries" vs DG's
+ * "O(m^2 p^2d)"; the nonzero ratios of Tables 1-4). Host only (no device or context). mesh: as for hdg_plan
+ * (all pointers [host]; elem_begin / n_elem / elem_ndof / rank_elem_begin unused). dg_ndof [host, E]: the DG
+ * unknowns of each element, m n(p_K) with n(p) = (p+1)(p+2)/2 and m the number of equations (4 for 2D Euler /
+ * Navier-Stokes: the DG scheme has no gradient unknowns). Outputs [host]:
+ *   nnz_dg  = sum_K dg_ndof_K^2 + sum over faces with two elements of 2 dg_ndof_L dg_ndof_R;
+ *   nnz_hdg = sum over face rows f of sum over the faces f' of f's elements of face_ndof_f face_ndof_f'
+ *             (= plan.nvals of a single-rank plan: the block-CSR skeleton matrix K).
+ * Returns HDG_ERR_ARG on inconsistent arguments. */
+hdg_status hdg_nnz_counts(const hdg_mesh* mesh, const int32_t* dg_ndof, int64_t* nnz_dg, int64_t* nnz_hdg);
 
 /* Lowest local element with info != 0 (synchronizes stream). Returns HDG_OK with *elem = -1 if none, or
  * HDG_ERR_SINGULAR with the element (local index) and its info code ("singular local block -> diagnostic

@@ -125,6 +125,21 @@ def condense(ne, nf, blk: dict):
     return dict(S=S, g=g, LU=LU, piv=piv, info=info, off_S=offS, off_g=offG, off_LU=offLU, off_piv=offPiv)
 
 
+def condense_shifted(ne, nf, blk: dict, shift):
+    """Re-condensation (§8(f) NEXT #4): O1-O3 of A_e + diag(shift_e) — the definition written
+    out: the shift (packed like r_e) is added to a copy of each element's diagonal, then the plain condensation."""
+    ne = np.asarray(ne)
+    A = np.array(blk["A"], dtype=np.float64, copy=True)
+    oA, oR = blk["off_A"], blk["off_re"]
+    for e in range(len(ne)):
+        n = int(ne[e])
+        for i in range(n):
+            A[oA[e] + i * n + i] += shift[oR[e] + i]
+    b = dict(blk)
+    b["A"] = A
+    return condense(ne, nf, b)
+
+
 def symbolic(elem_face, face_elem, face_ndof, f0: int = 0, f1: int | None = None):
     """O4 symbolic over face rows [f0, f1): (row_ptr int32, col_idx int32, blk_off int64)."""
     ef, fe, fn = _c(elem_face, np.int32), _c(face_elem, np.int32), _c(face_ndof, np.int32)

@@ -75,6 +75,10 @@ def lib():
         L.hdg_plan.argtypes = [P, ctypes.POINTER(_Mesh), ctypes.POINTER(_PlanInfo), P]
         L.hdg_condense.restype = I32
         L.hdg_condense.argtypes = [P] + [P] * 10 + [P]
+        L.hdg_condense_shifted.restype = I32
+        L.hdg_condense_shifted.argtypes = [P] + [P] * 11 + [P]
+        L.hdg_nnz_counts.restype = I32
+        L.hdg_nnz_counts.argtypes = [ctypes.POINTER(_Mesh), P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.hdg_assemble_skeleton.restype = I32
         L.hdg_assemble_skeleton.argtypes = [P] + [P] * 8 + [P]
         L.hdg_exchange_counts.restype = I32
@@ -108,7 +112,7 @@ EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status
             "hdg_ctx_destroy", "hdg_last_error", "hdg_plan", "hdg_condense", "hdg_assemble_skeleton",
             "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
             "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout", "hdg_condense_adjoint_rhs",
-            "hdg_assemble_adjoint", "hdg_backsubstitute_adjoint")
+            "hdg_assemble_adjoint", "hdg_backsubstitute_adjoint", "hdg_condense_shifted", "hdg_nnz_counts")
 
 
 def _ptr(t):
@@ -257,6 +261,13 @@ class Context:
         self._check(self._L.hdg_condense(self._h, *map(_ptr, (A, B, C, D, r_e, r_f, S, g, factors, info)),
                                          _stream(stream)), "hdg_condense")
 
+    def condense_shifted(self, A, B, C, D, r_e, r_f, shift, S, g, factors, info, stream=None):
+        """Re-condensation of A_e + diag(shift_e) (shift packed like r_e): the pseudo-time term M_e / dt_K of
+        PAPER.md:303-313 with an orthonormal basis (§8(f) NEXT #4)."""
+        _f64(A, B, C, D, r_e, r_f, shift, S, g)
+        self._check(self._L.hdg_condense_shifted(self._h, *map(_ptr, (A, B, C, D, r_e, r_f, shift, S, g, factors,
+                                                                      info)), _stream(stream)), "hdg_condense_shifted")
+
     # -- a6 / a7 ---------------------------------------------------------------------------------------------------
     def assemble_skeleton(self, S, g, K, E, row_ptr=None, col_idx=None, blk_off=None, send=None, stream=None):
         _f64(S, g, K, E, send)
@@ -344,6 +355,23 @@ def exchange_layout(elem_face, face_elem, face_ndof, elem_ndof, rank_elem_begin,
         raise HDGError(st, "hdg_exchange_layout")
     return dict(send_counts=arrs[0], send_displs=arrs[1], recv_counts=arrs[2], recv_displs=arrs[3], send_items=si,
                 recv_items=ri)
+
+
+def nnz_counts(elem_face, face_elem, face_ndof, dg_ndof):
+    """hdg_nnz_counts (host only): (nonzeros of the DG system matrix, nonzeros of the HDG skeleton matrix K) for the
+    mesh; dg_ndof[e] = m n(p_e) DG unknowns per element (§8(f) NEXT #4, Tables 1-4)."""
+    L = lib()
+    ef = np.ascontiguousarray(elem_face, dtype=np.int32)
+    fe = np.ascontiguousarray(face_elem, dtype=np.int32)
+    fn = np.ascontiguousarray(face_ndof, dtype=np.int32)
+    dn = np.ascontiguousarray(dg_ndof, dtype=np.int32)
+    m = _Mesh(ef.shape[0], fe.shape[0], 0, ef.shape[0], ef.ctypes.data, fe.ctypes.data, fn.ctypes.data,
+              dn.ctypes.data, None)
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    st = L.hdg_nnz_counts(ctypes.byref(m), dn.ctypes.data, ctypes.byref(a), ctypes.byref(b))
+    if st != HDG_OK:
+        raise HDGError(st, "hdg_nnz_counts")
+    return a.value, b.value
 
 
 def exchange_buffers(send, recv, send_counts, send_displs, recv_counts, recv_displs, rank: int, nranks: int,

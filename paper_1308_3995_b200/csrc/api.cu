@@ -435,22 +435,24 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
   return HDG_OK;
 }
 
-hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
-                        const double* r_e, const double* r_f, double* S, double* g, void* factors, int32_t* info,
-                        hdg_stream stream) {
+static hdg_status condense_impl(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                                const double* r_e, const double* r_f, const double* shift, double* S, double* g,
+                                void* factors, int32_t* info, hdg_stream stream, const char* name) {
   if (!ctx) return HDG_ERR_ARG;
   const Plan& p = ctx->plan;
-  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_condense: no plan");
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "%s: no plan", name);
   ctx->launches = 0;
   if (p.n == 0) return HDG_OK;
   const void* ptrs[] = {A, B, C, D, r_e, r_f, S, g, factors, info};
   for (const void* q : ptrs)
-    if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "hdg_condense: null or misaligned (16 B) pointer");
+    if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "%s: null or misaligned (16 B) pointer", name);
+  if (shift && !aligned16(shift)) return fail(ctx, HDG_ERR_ARG, "%s: misaligned (16 B) shift", name);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   HDG_CUDA(ctx, cudaSetDevice(ctx->device));
   for (const Bucket& b : p.buckets) {
     CondenseArgs a;
     a.A = A; a.B = B; a.C = C; a.D = D; a.re = r_e; a.rf = r_f; a.S = S; a.g = g;
+    a.shift = shift;
     a.factors = static_cast<unsigned char*>(factors);
     a.info = info;
     a.elems = b.d_elems;
@@ -469,6 +471,18 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
     else HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
   }
   return HDG_OK;
+}
+
+hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                        const double* r_e, const double* r_f, double* S, double* g, void* factors, int32_t* info,
+                        hdg_stream stream) {
+  return condense_impl(ctx, A, B, C, D, r_e, r_f, nullptr, S, g, factors, info, stream, "hdg_condense");
+}
+
+hdg_status hdg_condense_shifted(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                                const double* r_e, const double* r_f, const double* shift, double* S, double* g,
+                                void* factors, int32_t* info, hdg_stream stream) {
+  return condense_impl(ctx, A, B, C, D, r_e, r_f, shift, S, g, factors, info, stream, "hdg_condense_shifted");
 }
 
 hdg_status hdg_assemble_skeleton(hdg_ctx ctx, const double* S, const double* g, int32_t* row_ptr, int32_t* col_idx,
@@ -658,4 +672,47 @@ hdg_status hdg_exchange_layout(const hdg_mesh* m, int rank, int nranks, int64_t*
   return HDG_OK;
 }
 
+// ---- §8(f) NEXT #4: DG-vs-HDG global-matrix size (Tables 1-4 "nonzero ratios"; SPEC.md dg_nnz) ---
+hdg_status hdg_nnz_counts(const hdg_mesh* m, const int32_t* dg_ndof, int64_t* nnz_dg, int64_t* nnz_hdg) {
+  if (!m || !m->elem_face || !m->face_elem || !m->face_ndof || !dg_ndof || !nnz_dg || !nnz_hdg) return HDG_ERR_ARG;
+  const int64_t E = m->n_elem_global, F = m->n_face;
+  if (E < 0 || F < 0) return HDG_ERR_ARG;
+  for (int64_t i = 0; i < 3 * E; ++i)
+    if (m->elem_face[i] < -1 || m->elem_face[i] >= F) return HDG_ERR_ARG;
+  for (int64_t f = 0; f < F; ++f) {
+    const int32_t l = m->face_elem[2 * f], r = m->face_elem[2 * f + 1];
+    if (l < 0 || l >= E || r >= E || m->face_ndof[f] <= 0) return HDG_ERR_ARG;
+  }
+  // DG (element unknowns coupled through interior faces): one diagonal block per element and one block per
+  // neighbour pair in each direction
+  int64_t dg = 0;
+  for (int64_t e = 0; e < E; ++e) dg += (int64_t)dg_ndof[e] * dg_ndof[e];
+  for (int64_t f = 0; f < F; ++f) {
+    const int32_t l = m->face_elem[2 * f], r = m->face_elem[2 * f + 1];
+    if (r >= 0) dg += 2 * (int64_t)dg_ndof[l] * dg_ndof[r];
+  }
+  // HDG skeleton (trace unknowns): block row f couples the faces of its one or two elements (diagonal included)
+  int64_t hdg = 0;
+  for (int64_t f = 0; f < F; ++f) {
+    int32_t cols[6];
+    int nc = 0;
+    for (int side = 0; side < 2; ++side) {
+      const int32_t e = m->face_elem[2 * f + side];
+      if (e < 0) continue;
+      for (int k = 0; k < 3; ++k) {
+        const int32_t c = m->elem_face[3 * e + k];
+        if (c < 0) continue;
+        bool seen = false;
+        for (int q = 0; q < nc; ++q) seen |= cols[q] == c;
+        if (!seen) cols[nc++] = c;
+      }
+    }
+    for (int q = 0; q < nc; ++q) hdg += (int64_t)m->face_ndof[f] * m->face_ndof[cols[q]];
+  }
+  *nnz_dg = dg;
+  *nnz_hdg = hdg;
+  return HDG_OK;
+}
+
 }  // extern "C"
+

@@ -476,7 +476,7 @@ __device__ __forceinline__ bool phase_a(double* T, const Geo& geo, double* Uinv_
 
 template <int NWARPS>
 __device__ __forceinline__ void stage(double* T, const Geo& geo, const double* A, const double* Bm, const double* re,
-                                      int warp, int lane) {
+                                      const double* sh, int warp, int lane) {
   const int ne = geo.ne, nf = geo.nf, R = geo.R8, CB = geo.CB, C8 = geo.C8, ldT = geo.ldT;
   for (int i = warp; i < R; i += NWARPS) {
     double* Ti = T + i * ldT;
@@ -488,6 +488,10 @@ __device__ __forceinline__ void stage(double* T, const Geo& geo, const double* A
       for (int j = lane; j < nf / 2; j += 32) reinterpret_cast<double2*>(Ti + CB)[j] = __ldg(Bi + j);
       if (lane == 0) Ti[CB + nf] = __ldg(re + i);
       for (int j = CB + nf + 1 + lane; j < C8; j += 32) Ti[j] = 0.0;
+      if (sh) {   // re-condensation: the diagonal shift of row i
+        __syncwarp();
+        if (lane == 0) Ti[i] += __ldg(sh + i);
+      }
     } else {
       for (int j = lane; j < C8; j += 32) Ti[j] = 0.0;
     }
@@ -628,7 +632,8 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
     const int64_t next = it + gridDim.x;
 
     // ---- a1 stage + a2 (+ forward part of a3) --------------------------------------------------------------
-    if (!T_SMEM) stage<NWARPS>(T, geo, A, Bm, re, warp, lane);
+    const double* sh = a.shift ? a.shift + a.offRe[l] : nullptr;
+    if (!T_SMEM) stage<NWARPS>(T, geo, A, Bm, re, sh, warp, lane);
     if (tid == 0) { *flag = 0; *spec = 0; }
     const int64_t tit = (it - blockIdx.x) / gridDim.x;
     // phase B reads C_e, D_e, r_f long after they are needed by nothing else: pull them into L2 now
@@ -637,7 +642,11 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
       prefetch_l2(a.D + a.offD[l], (uint32_t)(nf * nf * 8));
     }
     HDG_STAMP(a.trace, tit, 0);
-    if (T_SMEM) mbar_wait(&mbar[0], ph);
+    if (T_SMEM) {
+      mbar_wait(&mbar[0], ph);
+      if (sh)
+        for (int i = tid; i < ne; i += THREADS) T[i * ldT + i] += __ldg(sh + i);   // before the barrier below
+    }
     HDG_STAMP(a.trace, tit, 1);
     __syncthreads();
     HDG_STAMP(a.trace, tit, 2);
@@ -646,7 +655,7 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
                                 T_SMEM ? &mbar[1] : nullptr, ph, a.trace, tit)) {
       pivoted = true;
       __syncthreads();
-      stage<NWARPS>(T, geo, A, Bm, re, warp, lane);
+      stage<NWARPS>(T, geo, A, Bm, re, sh, warp, lane);
       if (tid == 0) { *flag = 0; *spec = 0; }
       __syncthreads();
       phase_a<true, NWARPS>(T, geo, Uinv_all, Linv, piv, flag, spec, tid, warp, lane);

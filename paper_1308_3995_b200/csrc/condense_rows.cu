@@ -290,6 +290,10 @@ __global__ void __launch_bounds__(NWARPS * 32, 1) rows_kernel(const CondenseArgs
       for (int j = 0; j < NCTM; ++j) {
         const int c0 = 8 * j + 2 * tig;
         if (real && c0 - RA == nf) x[j][0] = vlast;                       // the r_e / r_f column
+        if (isA && real && a.shift) {                                     // re-condensation: A_e + diag(shift_e)
+          if (c0 == r) x[j][0] += __ldg(a.shift + a.offRe[l] + r);
+          if (c0 + 1 == r) x[j][1] += __ldg(a.shift + a.offRe[l] + r);
+        }
         if (isA && !real) {                                               // identity padding rows of A
           x[j][0] = c0 == r ? 1.0 : 0.0;
           x[j][1] = c0 + 1 == r ? 1.0 : 0.0;

@@ -460,14 +460,14 @@ struct Region {
 // exact path: unblocked GEPP over [T | Cr] by the whole CTA (taken only when the speculation fails)
 template <int THREADS>
 __device__ void sweep_pivot(double* T, double* Cr, const SweepGeo& G, const double* A, const double* Bm,
-                            const double* re, const double* Cm, int* piv, int* shared_fail, int tid) {
+                            const double* re, const double* Cm, const double* sh, int* piv, int* shared_fail, int tid) {
   const int ne = G.ne, nf = G.nf, ldT = G.ldT, ldC = G.ldC, CB = G.CB, NC = G.NCAB;
-  // restage from global (zero padding everywhere)
+  // restage from global (zero padding everywhere); sh: the diagonal shift (re-condensation), NULL = none
   for (int i = tid; i < G.RA * ldT; i += THREADS) {
     const int row = i / ldT, col = i - row * ldT;
     double v = 0.0;
     if (row < ne) {
-      if (col < ne) v = A[(size_t)row * ne + col];
+      if (col < ne) v = A[(size_t)row * ne + col] + ((sh && col == row) ? sh[row] : 0.0);
       else if (col >= CB && col < CB + nf) v = Bm[(size_t)row * nf + col - CB];
       else if (col == CB + nf) v = re[row];
     }
@@ -541,14 +541,15 @@ __device__ void sweep_pivot(double* T, double* Cr, const SweepGeo& G, const doub
 // both roles call it.
 template <int THREADS>
 __device__ __noinline__ void exact_element(const double* A, const double* Bm, const double* re, const double* Cm,
-                                           const double* D, const double* rf, double* S, double* g, double* LU,
-                                           int32_t* info, int ne, int nf, double* X, int* piv, int* sfail, int tid) {
+                                           const double* D, const double* rf, const double* sh, double* S, double* g,
+                                           double* LU, int32_t* info, int ne, int nf, double* X, int* piv, int* sfail,
+                                           int tid) {
   const SweepGeo G(ne, nf);
   const int ldT = G.ldT, ldC = G.ldC, CB = G.CB;
   double* T = X;
   double* Cr = X + (size_t)G.RA * ldT;
   __syncthreads();
-  sweep_pivot<THREADS>(T, Cr, G, A, Bm, re, Cm, piv, sfail, tid);
+  sweep_pivot<THREADS>(T, Cr, G, A, Bm, re, Cm, sh, piv, sfail, tid);
   const int fail = *sfail;
   if (fail) {
     for (int i = tid; i < nf * nf; i += THREADS) S[i] = __longlong_as_double(0x7ff8000000000000LL);
@@ -652,9 +653,15 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     const double2* Bm = reinterpret_cast<const double2*>(a.B + a.offB[l]);
     const double2* Cm = reinterpret_cast<const double2*>(a.C + a.offC[l]);
     const int ha = ne >> 1, hf = nf >> 1;
+    const double* sh = a.shift ? a.shift + a.offRe[l] : nullptr;
     for (int q = tid; q < ne * ha; q += THREADS) {
       const int i = q / ha, j = q - i * ha;
-      *reinterpret_cast<double2*>(T + (size_t)i * ldT + 2 * j) = __ldg(A + q);
+      double2 v = __ldg(A + q);
+      if (sh && (i >> 1) == j) {   // the diagonal entry of row i is in this pair
+        if (i & 1) v.y += __ldg(sh + i);
+        else v.x += __ldg(sh + i);
+      }
+      *reinterpret_cast<double2*>(T + (size_t)i * ldT + 2 * j) = v;
     }
     for (int q = tid; q < ne * hf; q += THREADS) {
       const int i = q / hf, j = q - i * hf;
@@ -664,6 +671,12 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       const int i = q / ha, j = q - i * ha;
       *reinterpret_cast<double2*>(Cr + (size_t)i * ldC + 2 * j) = __ldg(Cm + q);
     }
+  };
+  // re-condensation: one warp adds element l's diagonal shift to rows [r_lo, r_hi) of T once they have landed
+  auto shift_rows = [&](int64_t l, int r_lo, int r_hi) {
+    const double* sh = a.shift + a.offRe[l];
+    for (int i = r_lo + lane; i < r_hi; i += 32) T[(size_t)i * ldT + i] += __ldg(sh + i);
+    __syncwarp();
   };
   auto prefetch = [&](int64_t l) {
     prefetch_l2(a.A + a.offA[l], (uint32_t)(ne * ne * 8));
@@ -707,7 +720,10 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         double* LUd = LU;
         bool do_diag = true;
         if (p < 0) {
-          if (!GT) mbar_wait(&mbar[0], ph);
+          if (!GT) {
+            mbar_wait(&mbar[0], ph);
+            if (a.shift) shift_rows(l, 0, r1);   // the chain warp's first diagonal block: its rows' shift
+          }
         } else {
           if (__syncthreads_or(viol)) { aborted = true; break; }
           SW_STAMP(tit, 8 + 4 * p);
@@ -728,6 +744,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
             // the next element's first diagonal block, overlapped with the workers' last-panel work
             // (npan == 1: its rows arrive only after barrier F)
             mbar_wait(&mbar[0], ph ^ 1u);
+            if (a.shift) shift_rows(elem_of(next), 0, r1);
             LUd = reinterpret_cast<double*>(a.factors + a.offF[elem_of(next)]);
             dbuf = buf ^ 1;
             early = true;
@@ -753,7 +770,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         ++pc;   // the aborted panel's buffer may be half-written
         __syncthreads();   // A: remaining loads of the next element issued by the loader warp
         exact_element<THREADS>(a.A + a.offA[l], a.B + a.offB[l], a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l],
-                                a.rf + a.offRf[l], a.S + a.offS[l], a.g + a.offG[l],
+                                a.rf + a.offRf[l], a.shift ? a.shift + a.offRe[l] : nullptr, a.S + a.offS[l],
+                                a.g + a.offG[l],
                                 reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, ne, nf, X, piv, sfail,
                                 tid);
       } else {
@@ -818,6 +836,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       if (!GT) mbar_wait(&mbar[0], ph);
       SW_STAMP(tit, 5);
       if (!GT) mbar_wait(&mbar[1], ph);
+      if (!GT && a.shift && helper) shift_rows(l, r1, ne);   // before the first panel barrier: no reader yet
       SW_STAMP(tit, 3);
       bool viol = false;
       bool aborted = false;
@@ -933,7 +952,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         }
         __syncthreads();   // A
         exact_element<THREADS>(a.A + a.offA[l], a.B + a.offB[l], a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l],
-                                a.rf + a.offRf[l], a.S + a.offS[l], a.g + a.offG[l],
+                                a.rf + a.offRf[l], a.shift ? a.shift + a.offRe[l] : nullptr, a.S + a.offS[l],
+                                a.g + a.offG[l],
                                 reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, ne, nf, X, piv, sfail,
                                 tid);
       } else {
@@ -1007,7 +1027,8 @@ __global__ void __launch_bounds__(THREADS) exact_list_kernel(const CondenseArgs 
   for (int q = blockIdx.x; q < n; q += gridDim.x) {
     const int64_t l = list[q];
     exact_element<THREADS>(a.A + a.offA[l], a.B + a.offB[l], a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l],
-                           a.rf + a.offRf[l], a.S + a.offS[l], a.g + a.offG[l],
+                           a.rf + a.offRf[l], a.shift ? a.shift + a.offRe[l] : nullptr, a.S + a.offS[l],
+                           a.g + a.offG[l],
                            reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, a.ne, a.nf, X, piv, sfail,
                            threadIdx.x);
   }

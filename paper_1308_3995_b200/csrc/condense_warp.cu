@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
     const double* A = a.A + a.offA[l];
     const double* Bm = a.B + a.offB[l];
     const double* re = a.re + a.offRe[l];
+    const double* sh = a.shift ? a.shift + a.offRe[l] : nullptr;   // re-condensation: A_e + diag(shift_e)
     // ---- T = [A | B r], row by row (consecutive lanes read consecutive entries of a row) -----------------------
     // (eight rows of loads in flight before their shared-memory stores: the generic T pointer could alias the
     // global inputs as far as the compiler knows, so load/store pairs would otherwise serialise)
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
       for (int q = 0; q < 8; ++q) {
         const int i = i0 + q;
         const bool rv = i < ne;
-        v0[q] = (rv && c0 < ne) ? __ldg(A + i * ne + c0)
+        v0[q] = (rv && c0 < ne) ? __ldg(A + i * ne + c0) + ((sh && c0 == i) ? __ldg(sh + i) : 0.0)
                                 : ((rv && c0 < ne + nf) ? __ldg(Bm + i * nf + c0 - ne) : ((rv && c0 == ne + nf) ? __ldg(re + i) : 0.0));
         v1[q] = (rv && c1 < ne + nf) ? __ldg(Bm + i * nf + c1 - ne) : ((rv && c1 == ne + nf) ? __ldg(re + i) : 0.0);
       }

@@ -77,6 +77,7 @@ __host__ __device__ inline int64_t factor_bytes(int ne) { return ((int64_t)ne * 
 
 struct CondenseArgs {
   const double *A, *B, *C, *D, *re, *rf;
+  const double* shift;    // NULL, or per-element diagonal shift packed like r_e: A_e + diag(shift_e) is condensed
   double *S, *g;
   unsigned char* factors;
   int32_t* info;
