@@ -219,15 +219,48 @@ class ClockSampler:
         return out
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def slab_bounds(E: int, n: int):
     return np.array([(r * E) // n for r in range(n + 1)], dtype=np.int64)
 
 
-def oracle_sample(w, seconds: float, lam, max_elems=None):
+def _omp_threads(n=None):
+    """OpenMP thread count of this process (the oracle's parallel loops): set it when n is given, return the
+    previous value. Plumbing for the 1-thread oracle number; the oracle is not modified."""
+    import ctypes
+    try:
+        gomp = ctypes.CDLL("libgomp.so.1")
+    except OSError:
+        return None
+    prev = gomp.omp_get_max_threads()
+    if n is not None:
+        gomp.omp_set_num_threads(int(n))
+    return prev
+
+
+def oracle_sample(w, seconds: float, lam, max_elems=None, threads=None):
     """The oracle (as it stands) on a bounded sample of the workload: condense + assemble (rows owned by the
-    sample) + back-substitute for the first m elements. Returns (elements/s, m, wall seconds, threads)."""
+    sample) + back-substitute for the first m elements. Returns (elements/s, m, wall seconds, threads).
+    threads: OpenMP threads for this sample (None: all the host cores, the default)."""
     import oracle
     import gen
+    if threads is not None:
+        prev = _omp_threads(threads)
+        try:
+            v = oracle_sample(w, seconds, lam, max_elems)
+        finally:
+            if prev:
+                _omp_threads(prev)
+        return v[0], v[1], v[2], threads
 
     def run(m):
         blk = gen.host_blocks(w, 0, m)
@@ -247,7 +280,7 @@ def oracle_sample(w, seconds: float, lam, max_elems=None):
     if max_elems:
         m2 = min(m2, max_elems)
     t2 = run(m2)
-    threads = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    threads = _omp_threads() or int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
     return m2 / t2, m2, t2, threads
 
 
@@ -508,6 +541,13 @@ def run_step(wl, ev=None):
     ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], wl["S"], wl["g"], wl["F"], wl["infot"],
                  stream=stream)
     n += ctx.launch_count()
+    if wl.get("X") is not None:
+        if ev:
+            ev[4].record(stream)
+        ctx.save_solutions(wl["F"], inp["B"], inp["re"], wl["X"], stream=stream)
+        n += ctx.launch_count()
+        if ev:
+            ev[5].record(stream)
     if ev:
         ev[1].record(stream)
     ctx.assemble_skeleton(wl["S"], wl["g"], wl["K"], wl["E"], send=wl["send"], stream=stream)
@@ -518,7 +558,12 @@ def run_step(wl, ev=None):
         n += ctx.launch_count()
     if ev:
         ev[2].record(stream)
-    ctx.backsubstitute(wl["F"], inp["B"], inp["re"], wl["lam"], wl["u"], stream=stream)
+    if wl.get("X") is not None:
+        # §8(f) NEXT #2: the local solutions were saved after the condensation (ev[4]..ev[5]);
+        # the reconstruction is a GEMV on them
+        ctx.backsubstitute_saved(wl["X"], wl["lam"], wl["u"], stream=stream)
+    else:
+        ctx.backsubstitute(wl["F"], inp["B"], inp["re"], wl["lam"], wl["u"], stream=stream)
     n += ctx.launch_count()
     if ev:
         ev[3].record(stream)
@@ -536,8 +581,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--path", default="primal", choices=["primal", "adjoint"],
-                    help="adjoint: time the transposed path (SURVEY.md §8(f) NEXT #1) on the primal factors")
+    ap.add_argument("--path", default="primal", choices=["primal", "adjoint", "saved"],
+                    help="adjoint: time the transposed path (SURVEY.md §8(f) NEXT #1) on the primal factors; saved: "
+                         "save the local solutions after the condensation and reconstruct from them (NEXT #2)")
+    ap.add_argument("--graph", type=int, default=0,
+                    help="also time G back-to-back steps captured in one CUDA graph (launch latency; C1/C2)")
     ap.add_argument("--slab", default=None,
                     help="r/P: time rank r's slab of a P-way partition on this one GPU (default for C5: 0/8)")
     args = ap.parse_args()
@@ -568,6 +616,8 @@ def main():
     wl = setup_workload(args.config, rank, world, local, slab=args.slab)
     if args.path == "adjoint":
         return run_adjoint(args, wl, rank, world, local)
+    if args.path == "saved":
+        wl["X"] = wl["ctx"].alloc("X")
     w, ctx, info, stream, inp, lam = wl["w"], wl["ctx"], wl["info"], wl["stream"], wl["inp"], wl["lam"]
     S, g, u, F, infot, K, E, send, recv = (wl[k] for k in ("S", "g", "u", "F", "infot", "K", "E", "send", "recv"))
     eb, n, reb = wl["eb"], wl["n"], wl["reb"]
@@ -597,7 +647,7 @@ def main():
     if bad >= 0:
         raise RuntimeError(f"singular element {bad} (info {code}) in the benchmark inputs")
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -616,12 +666,35 @@ def main():
     cond_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     asm_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     bs_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    save_ms = (sum(e[4].elapsed_time(e[5]) for e in evs) / args.steps) if args.path == "saved" else 0.0
     gpu_launches = launches[0]
-    t = torch.tensor([total_ms, cond_ms, asm_ms, bs_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, cond_ms, asm_ms, bs_ms, save_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, cond_ms, asm_ms, bs_ms = t.tolist()
+    total_ms, cond_ms, asm_ms, bs_ms, save_ms = t.tolist()
+    cond_ms -= save_ms       # (ev[1] follows the save in the saved path)
     ms_step = total_ms / args.steps
+
+    # ---- CUDA graph of G back-to-back steps (no flush between them): separates launch latency
+    graph = None
+    if args.graph > 0:
+        g_ = torch.cuda.CUDAGraph()
+        run_step(wl)                      # warm (kernel attributes set outside the capture)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g_, stream=stream):
+            for _ in range(args.graph):
+                run_step(wl)
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):     # replay() launches on the current stream: make it the timed one
+            g_.replay()
+            torch.cuda.synchronize()
+            a_.record(stream)
+            g_.replay()
+            b_.record(stream)
+        torch.cuda.synchronize()
+        gms = a_.elapsed_time(b_) / args.graph
+        graph = {"steps_in_graph": args.graph, "ms_per_step": gms, "value": elems / (gms * 1e-3),
+                 "unit": "elements/s", "note": "back to back inside one CUDA graph, L2 not flushed between steps"}
 
     # ---- e2e: the same step through the public API with HOST buffers (pinned), copies inside the timed region ----
     e2e = None
@@ -669,9 +742,13 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, m, secs, threads = oracle_sample(w, args.cpu_seconds, gen.host_lambda(w))
+        v1, m1, secs1, _ = oracle_sample(w, 3.0, gen.host_lambda(w), threads=1)
         cpu = {"value": v, "unit": "elements/s", "cores": threads, "kind": "oracle",
                "sample": f"first {m} of {w.E} elements: oracle condense + assemble (rows owned by the sample) + "
-                         f"back-substitute, {secs:.1f} s wall, generation excluded"}
+                         f"back-substitute, {secs:.1f} s wall, generation excluded",
+               "one_thread": {"value": v1, "unit": "elements/s", "cores": 1,
+                              "sample": f"first {m1} elements, {secs1:.1f} s wall, 1 OpenMP thread"},
+               "host_cpu": _cpu_model()}
 
     if rank == 0:
         work = algorithmic(w.elem_ne[eb:eb + n], w.elem_nf[eb:eb + n])
@@ -722,10 +799,16 @@ def main():
             "condense_per_s": elems / (cond_ms * 1e-3), "backsub_per_s": elems / (bs_ms * 1e-3),
             "condense_ms": cond_ms, "assemble_ms": asm_ms, "backsub_ms": bs_ms,
             "backsub_hbm_gbs": work["backsub_bytes"] / (bs_ms * 1e-3) / 1e9,
+            **({"path": "saved", "save_solutions_ms": save_ms,
+                "backsub_saved_bytes": float(sum(8 * int(a) * (int(b) + 1) + 8 * int(b) + 8 * int(a) for a, b in
+                                                 zip(w.elem_ne[eb:eb + n], w.elem_nf[eb:eb + n]))),
+                "note": "condense_ms excludes hdg_save_solutions (save_solutions_ms); backsub_ms is the GEMV on "
+                        "the saved X (backsub_saved_bytes: X, lambda_e gather, u)"} if args.path == "saved" else {}),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
+            **({"cuda_graph": graph} if graph else {}),
             "clocks": clk,
             "fp64_peak_tflops": {"dmma": dmma_peak, "dfma": dfma_peak},
         }

@@ -113,6 +113,7 @@ typedef struct {
   int32_t n_buckets;                    /* distinct (n_e, n_f) classes among local elements */
   int32_t max_ne, max_nf;
   int64_t send_doubles, recv_doubles;   /* exchange buffer sizes (0 when nranks == 1) */
+  int64_t len_X;                        /* doubles of the saved local solutions (hdg_save_solutions) */
 } hdg_plan_info;
 
 /* a0 plan (once per mesh and degree map): validates the mesh, buckets local elements by (n_e, n_f) (the hp
@@ -188,6 +189,22 @@ hdg_status hdg_skeleton_accumulate(hdg_ctx ctx, const double* recv, double* K, d
  * factors: from hdg_condense on the same plan. B, r_e: the packed inputs of hdg_condense. u: packed output. */
 hdg_status hdg_backsubstitute(hdg_ctx ctx, const void* factors, const double* B, const double* r_e,
                               const double* lambda, double* u, hdg_stream stream);
+
+/* ---- saved local solutions: SURVEY.md §8(f) NEXT #2 ----------------------------------------------------------
+ * "the solutions to Eq. (ls) can be saved after the assembly of the hybridized system and reused during the
+ * reconstruction". X_e = A_e^-1 [B_e | r_e]: n_e x (n_f + 1) row-major per element, packed densely
+ * in local element order (plan.len_X doubles in total); its last column is y_e = A_e^-1 r_e. */
+
+/* X_e = A_e^-1 [B_e | r_e] for every local element from the saved factors (P A_e = L U: permute, forward, backward
+ * solves of the n_f + 1 right-hand sides on the FP64 tensor cores). factors, B, r_e: as for hdg_backsubstitute.
+ * X: device output (plan.len_X doubles, 16-byte aligned). */
+hdg_status hdg_save_solutions(hdg_ctx ctx, const void* factors, const double* B, const double* r_e, double* X,
+                              hdg_stream stream);
+
+/* Reconstruction from the saved solutions: u_e = y_e - X_e[:, 0:n_f] lambda_e (= A_e^-1 (r_e - B_e lambda_e)),
+ * a GEMV per element reading n_e (n_f + 1) doubles instead of the factors, B_e and r_e. lambda as for
+ * hdg_backsubstitute; u packed like hdg_backsubstitute's. */
+hdg_status hdg_backsubstitute_saved(hdg_ctx ctx, const double* X, const double* lambda, double* u, hdg_stream stream);
 
 /* ---- adjoint (transposed) use of the same factors: SURVEY.md §8(f) NEXT #1, PAPER.md:414-436 ----------------
  * The adjoint local matrix is the transpose of the primal one and the hybridized adjoint matrix

@@ -140,6 +140,43 @@ def condense_shifted(ne, nf, blk: dict, shift):
     return condense(ne, nf, b)
 
 
+def save_solutions(ne, nf, c: dict, blk: dict):
+    """§8(f) NEXT #2: the saved local solutions X_e = A_e^-1 [B_e | r_e] (n_e x (n_f + 1) row-major,
+    packed per element) by O2 on each element's saved factors. Returns (X, off_X)."""
+    ne = np.asarray(ne, dtype=np.int64)
+    nf = np.asarray(nf, dtype=np.int64)
+    offX = _offsets(ne * (nf + 1))
+    X = np.empty(int(offX[-1]))
+    for e in range(len(ne)):
+        n, f = int(ne[e]), int(nf[e])
+        rhs = np.empty((n, f + 1))
+        rhs[:, :f] = np.asarray(blk["B"][blk["off_B"][e]:blk["off_B"][e + 1]]).reshape(n, f)
+        rhs[:, f] = blk["re"][blk["off_re"][e]:blk["off_re"][e + 1]]
+        LU = np.asarray(c["LU"][c["off_LU"][e]:c["off_LU"][e + 1]]).reshape(n, n)
+        piv = c["piv"][c["off_piv"][e]:c["off_piv"][e + 1]]
+        X[offX[e]:offX[e + 1]] = lu_solve(LU, piv, rhs).ravel()
+    return X, offX
+
+
+def backsub_saved(elem_face, face_ndof, face_off, ne, nf, X, offX, lam, e0: int = 0):
+    """Reconstruction from the saved solutions: u_e = y_e - X_e[:, :n_f] lambda_e (y_e = X_e's last column),
+    lambda_e gathered in slot order as O6; the sum ascending. Returns (u, off_u)."""
+    ne = np.asarray(ne, dtype=np.int64)
+    offU = _offsets(ne)
+    u = np.empty(int(offU[-1]))
+    for l in range(len(ne)):
+        n, f = int(ne[l]), int(nf[l])
+        lam_e = np.concatenate([np.asarray(lam[int(face_off[q]):int(face_off[q]) + int(face_ndof[q])])
+                                for q in elem_face[e0 + l] if q >= 0]) if f else np.zeros(0)
+        Xe = np.asarray(X[offX[l]:offX[l + 1]]).reshape(n, f + 1)
+        for i in range(n):
+            acc = 0.0
+            for j in range(f):
+                acc = acc + Xe[i, j] * lam_e[j]
+            u[offU[l] + i] = Xe[i, f] - acc
+    return u, offU
+
+
 def symbolic(elem_face, face_elem, face_ndof, f0: int = 0, f1: int | None = None):
     """O4 symbolic over face rows [f0, f1): (row_ptr int32, col_idx int32, blk_off int64)."""
     ef, fe, fn = _c(elem_face, np.int32), _c(face_elem, np.int32), _c(face_ndof, np.int32)

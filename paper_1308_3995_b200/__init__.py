@@ -44,7 +44,7 @@ class _PlanInfo(ctypes.Structure):
         "factor_bytes", "owned_face_begin", "n_owned_faces", "nnzb", "nvals", "owned_trace_begin",
         "n_owned_trace", "n_trace")] + [("n_buckets", ctypes.c_int32), ("max_ne", ctypes.c_int32),
                                         ("max_nf", ctypes.c_int32), ("send_doubles", ctypes.c_int64),
-                                        ("recv_doubles", ctypes.c_int64)]
+                                        ("recv_doubles", ctypes.c_int64), ("len_X", ctypes.c_int64)]
 
 
 _lib = None
@@ -77,6 +77,10 @@ def lib():
         L.hdg_condense.argtypes = [P] + [P] * 10 + [P]
         L.hdg_condense_shifted.restype = I32
         L.hdg_condense_shifted.argtypes = [P] + [P] * 11 + [P]
+        L.hdg_save_solutions.restype = I32
+        L.hdg_save_solutions.argtypes = [P] + [P] * 4 + [P]
+        L.hdg_backsubstitute_saved.restype = I32
+        L.hdg_backsubstitute_saved.argtypes = [P] + [P] * 3 + [P]
         L.hdg_nnz_counts.restype = I32
         L.hdg_nnz_counts.argtypes = [ctypes.POINTER(_Mesh), P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.hdg_assemble_skeleton.restype = I32
@@ -112,7 +116,8 @@ EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status
             "hdg_ctx_destroy", "hdg_last_error", "hdg_plan", "hdg_condense", "hdg_assemble_skeleton",
             "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
             "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout", "hdg_condense_adjoint_rhs",
-            "hdg_assemble_adjoint", "hdg_backsubstitute_adjoint", "hdg_condense_shifted", "hdg_nnz_counts")
+            "hdg_assemble_adjoint", "hdg_backsubstitute_adjoint", "hdg_condense_shifted", "hdg_nnz_counts",
+            "hdg_save_solutions", "hdg_backsubstitute_saved")
 
 
 def _ptr(t):
@@ -167,6 +172,7 @@ class PlanInfo:
     max_nf: int
     send_doubles: int
     recv_doubles: int
+    len_X: int
 
 
 def get_unique_id() -> bytes:
@@ -240,7 +246,7 @@ class Context:
         i, dev = self.info, torch.device("cuda", self.device)
         f64 = dict(dtype=torch.float64, device=dev)
         sizes = {"S": i.len_S, "g": i.len_g, "u": i.len_u, "K": i.nvals, "E": i.n_owned_trace,
-                 "send": i.send_doubles, "recv": i.recv_doubles}
+                 "send": i.send_doubles, "recv": i.recv_doubles, "X": i.len_X}
         if what in sizes:
             return torch.empty(max(sizes[what], 1), **f64)
         if what == "factors":
@@ -291,6 +297,19 @@ class Context:
         _f64(B, r_e, lam, u)
         self._check(self._L.hdg_backsubstitute(self._h, *map(_ptr, (factors, B, r_e, lam, u)), _stream(stream)),
                     "hdg_backsubstitute")
+
+    # ---- saved local solutions: SURVEY.md §8(f) NEXT #2, PAPER.md:359 ------------------------------------------------
+    def save_solutions(self, factors, B, r_e, X, stream=None):
+        """X_e = A_e^-1 [B_e | r_e] (n_e x (n_f + 1) row-major per element) from the saved factors."""
+        _f64(B, r_e, X)
+        self._check(self._L.hdg_save_solutions(self._h, *map(_ptr, (factors, B, r_e, X)), _stream(stream)),
+                    "hdg_save_solutions")
+
+    def backsubstitute_saved(self, X, lam, u, stream=None):
+        """u_e = y_e - X_e[:, :n_f] lambda_e from the saved solutions (a GEMV per element)."""
+        _f64(X, lam, u)
+        self._check(self._L.hdg_backsubstitute_saved(self._h, _ptr(X), _ptr(lam), _ptr(u), _stream(stream)),
+                    "hdg_backsubstitute_saved")
 
     # ---- adjoint (transposed) path: SURVEY.md §8(f) NEXT #1, PAPER.md:414-436 ---------------------------------------
     def condense_adjoint_rhs(self, factors, B, rt_e, rt_f, gt, stream=None):

@@ -307,14 +307,14 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
   }
 
   // ---- packed offsets --------------------------------------------------------------------------------------------
-  std::vector<std::vector<int64_t>> off(10, std::vector<int64_t>(n + 1, 0));
+  std::vector<std::vector<int64_t>> off(N_OFF, std::vector<int64_t>(n + 1, 0));
   for (int64_t l = 0; l < n; ++l) {
     const int64_t a = ne[l], f = nf[l];
-    const int64_t sz[10] = {a * a, a * f, f * a, f * f, a, f, f * f, f, a, factor_bytes((int)a)};
-    for (int k = 0; k < 10; ++k) off[k][l + 1] = off[k][l] + sz[k];
+    const int64_t sz[N_OFF] = {a * a, a * f, f * a, f * f, a, f, f * f, f, a, factor_bytes((int)a), a * (f + 1)};
+    for (int k = 0; k < N_OFF; ++k) off[k][l + 1] = off[k][l] + sz[k];
   }
-  p.len.resize(10);
-  for (int k = 0; k < 10; ++k) p.len[k] = off[k][n];
+  p.len.resize(N_OFF);
+  for (int k = 0; k < N_OFF; ++k) p.len[k] = off[k][n];
 
   // ---- buckets by (n_e, n_f), heaviest first ------------------------------------------------------------------
   std::map<std::pair<int, int>, std::vector<int32_t>> bk;
@@ -389,7 +389,7 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
   HDG_CUDA(ctx, upload(&p.d_face_off, face_off.data(), (size_t)(F + 1)));
   HDG_CUDA(ctx, upload(&p.d_ne, ne.data(), (size_t)n));
   HDG_CUDA(ctx, upload(&p.d_nf, nf.data(), (size_t)n));
-  for (int k = 0; k < 10; ++k) HDG_CUDA(ctx, upload(&p.d_off[k], off[k].data(), (size_t)(n + 1)));
+  for (int k = 0; k < N_OFF; ++k) HDG_CUDA(ctx, upload(&p.d_off[k], off[k].data(), (size_t)(n + 1)));
   {
     const cudaError_t e = skeleton_symbolic(p, s);
     if (e == cudaErrorMemoryAllocation) return fail(ctx, HDG_ERR_NOMEM, "hdg_plan: block-CSR structure: %s", cudaGetErrorString(e));
@@ -432,6 +432,7 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
   info->n_buckets = (int32_t)p.buckets.size();
   info->max_ne = p.max_ne; info->max_nf = p.max_nf;
   info->send_doubles = p.sk.send_doubles; info->recv_doubles = p.sk.recv_doubles;
+  info->len_X = p.len[OFF_X];
   return HDG_OK;
 }
 
@@ -714,5 +715,55 @@ hdg_status hdg_nnz_counts(const hdg_mesh* m, const int32_t* dg_ndof, int64_t* nn
   return HDG_OK;
 }
 
+// ---- §8(f) NEXT #2: saved local solutions ------------------------------------------------------
+static hdg_status solutions_call(hdg_ctx ctx, int mode, const char* name, const void* factors, const double* B,
+                                 const double* r_e, const double* X, const double* lambda, double* out,
+                                 hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "%s: no plan", name);
+  ctx->launches = 0;
+  if (p.n == 0) return HDG_OK;
+  const void* ptrs0[] = {factors, B, r_e, out};
+  const void* ptrs1[] = {X, out};
+  if (mode == 0) {
+    for (const void* q : ptrs0)
+      if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "%s: null or misaligned (16 B) pointer", name);
+  } else {
+    for (const void* q : ptrs1)
+      if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "%s: null or misaligned (16 B) pointer", name);
+    if (!lambda && p.n_trace > 0) return fail(ctx, HDG_ERR_ARG, "%s: null lambda", name);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  for (const Bucket& b : p.buckets) {
+    SolutionsArgs a{};
+    a.factors = static_cast<const unsigned char*>(factors);
+    a.B = B; a.re = r_e; a.lambda = lambda;
+    a.X = mode == 0 ? out : nullptr;
+    a.Xin = X;
+    a.u = mode == 1 ? out : nullptr;
+    a.elems = b.d_elems;
+    a.offB = p.d_off[OFF_B]; a.offRe = p.d_off[OFF_RE]; a.offF = p.d_off[OFF_F]; a.offX = p.d_off[OFF_X];
+    a.offU = p.d_off[OFF_U];
+    a.elem_face = p.d_elem_face; a.face_ndof = p.d_face_ndof; a.face_off = p.d_face_off;
+    a.elem_begin = p.eb;
+    a.ne = b.ne; a.nf = b.nf; a.count = b.count;
+    if (mode == 0) HDG_CUDA(ctx, launch_save_solutions(a, ctx->sms, s, &ctx->launches));
+    else HDG_CUDA(ctx, launch_backsub_saved(a, ctx->sms, s, &ctx->launches));
+  }
+  return HDG_OK;
+}
+
+hdg_status hdg_save_solutions(hdg_ctx ctx, const void* factors, const double* B, const double* r_e, double* X,
+                              hdg_stream stream) {
+  return solutions_call(ctx, 0, "hdg_save_solutions", factors, B, r_e, nullptr, nullptr, X, stream);
+}
+
+hdg_status hdg_backsubstitute_saved(hdg_ctx ctx, const double* X, const double* lambda, double* u, hdg_stream stream) {
+  return solutions_call(ctx, 1, "hdg_backsubstitute_saved", nullptr, nullptr, nullptr, X, lambda, u, stream);
+}
+
 }  // extern "C"
+
 

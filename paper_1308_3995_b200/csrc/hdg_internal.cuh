@@ -107,6 +107,23 @@ struct BacksubArgs {
   int64_t count;
 };
 
+// saved local solutions (§8(f) NEXT #2): X_e = A_e^-1 [B_e | r_e], n_e x (n_f + 1) row-major
+struct SolutionsArgs {
+  const unsigned char* factors;
+  const double *B, *re, *lambda;
+  double* X;          // hdg_save_solutions: output; hdg_backsubstitute_saved: input
+  const double* Xin;
+  double* u;
+  const int32_t* elems;
+  const int64_t *offB, *offRe, *offF, *offX, *offU;
+  const int32_t* elem_face;
+  const int32_t* face_ndof;
+  const int64_t* face_off;
+  int64_t elem_begin;
+  int ne, nf;
+  int64_t count;
+};
+
 struct AdjointArgs {
   const unsigned char* factors;
   const double *re, *rf, *M, *lambda;   // M = B_e (adjoint rhs) or C_e (adjoint reconstruction)
@@ -155,7 +172,7 @@ struct Plan {
   int32_t *d_elem_face = nullptr, *d_face_elem = nullptr, *d_face_ndof = nullptr;
   int64_t* d_face_off = nullptr;
   int32_t *d_ne = nullptr, *d_nf = nullptr;   // local elements
-  int64_t* d_off[10] = {};                     // A B C D re rf S g u F(bytes): [n+1] each
+  int64_t* d_off[11] = {};                     // A B C D re rf S g u F(bytes) X: [n+1] each
   std::vector<int64_t> len;                    // totals of the above
   std::vector<Bucket> buckets;
   Skeleton sk;
@@ -170,7 +187,7 @@ struct Plan {
   int64_t n_trace = 0;
 };
 
-enum { OFF_A = 0, OFF_B, OFF_C, OFF_D, OFF_RE, OFF_RF, OFF_S, OFF_G, OFF_U, OFF_F };
+enum { OFF_A = 0, OFF_B, OFF_C, OFF_D, OFF_RE, OFF_RF, OFF_S, OFF_G, OFF_U, OFF_F, OFF_X, N_OFF };
 
 }  // namespace hdg
 
@@ -200,6 +217,8 @@ cudaError_t launch_condense_rows(const CondenseArgs& a, int sms, size_t smem_opt
 cudaError_t launch_exact_list(const CondenseArgs& a, const int32_t* list, const int32_t* count, int grid, cudaStream_t s);
 cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_adjoint(const AdjointArgs& a, int mode, int sms, cudaStream_t s, int64_t* launches);
+cudaError_t launch_save_solutions(const SolutionsArgs& a, int sms, cudaStream_t s, int64_t* launches);
+cudaError_t launch_backsub_saved(const SolutionsArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s);
 cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, double* K, double* E, double* send,
                             cudaStream_t s, int64_t* launches, bool transposed = false);
