@@ -206,6 +206,23 @@ hdg_status hdg_save_solutions(hdg_ctx ctx, const void* factors, const double* B,
  * hdg_backsubstitute; u packed like hdg_backsubstitute's. */
 hdg_status hdg_backsubstitute_saved(hdg_ctx ctx, const double* X, const double* lambda, double* u, hdg_stream stream);
 
+/* ---- the skeleton solve: SURVEY.md §8(f) NEXT #3 ---------------------------------------------------------------
+ * "First, the hybridized system is assembled and then being solved for dLambda"; the paper uses an
+ * ILU(n)-preconditioned GMRES from PETSc. Here: restarted GMRES(restart), right-preconditioned
+ * with block Jacobi (the inverses of K's diagonal face blocks), all vector work in libhdg's kernels, deterministic
+ * reductions. Single rank (nranks == 1; HDG_ERR_UNSUPPORTED otherwise) and face trace sizes <= 24. */
+
+/* y = K x over the owned rows: x device [n_trace] (global trace numbering), y device [n_owned_trace]; K as filled by
+ * hdg_assemble_skeleton on this plan. Stream-ordered. */
+hdg_status hdg_skeleton_spmv(hdg_ctx ctx, const double* K, const double* x, double* y, hdg_stream stream);
+
+/* Solve K lambda = E: lambda device [n_trace], in: initial guess, out: the solution. Stops when the relative
+ * residual ||E - K lambda|| / ||E|| <= rtol (Arnoldi estimate; the true residual of the returned lambda is written
+ * to relres [host]) or after maxit iterations (iters [host]). Synchronizes the stream (the Hessenberg system lives on
+ * the host); the workspace ((restart + 1) n_trace doubles + the block inverses) is kept in the plan. */
+hdg_status hdg_skeleton_solve(hdg_ctx ctx, const double* K, const double* E, double* lambda, double rtol, int maxit,
+                              int restart, int* iters, double* relres, hdg_stream stream);
+
 /* ---- adjoint (transposed) use of the same factors: SURVEY.md §8(f) NEXT #1, PAPER.md:414-436 ----------------
  * The adjoint local matrix is the transpose of the primal one and the hybridized adjoint matrix
  * is K^T, so the adjoint reuses the plan and the factors of hdg_condense (same element degrees). */

@@ -81,6 +81,11 @@ def lib():
         L.hdg_save_solutions.argtypes = [P] + [P] * 4 + [P]
         L.hdg_backsubstitute_saved.restype = I32
         L.hdg_backsubstitute_saved.argtypes = [P] + [P] * 3 + [P]
+        L.hdg_skeleton_spmv.restype = I32
+        L.hdg_skeleton_spmv.argtypes = [P, P, P, P, P]
+        L.hdg_skeleton_solve.restype = I32
+        L.hdg_skeleton_solve.argtypes = [P, P, P, P, ctypes.c_double, I32, I32, ctypes.POINTER(I32),
+                                         ctypes.POINTER(ctypes.c_double), P]
         L.hdg_nnz_counts.restype = I32
         L.hdg_nnz_counts.argtypes = [ctypes.POINTER(_Mesh), P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.hdg_assemble_skeleton.restype = I32
@@ -117,7 +122,7 @@ EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status
             "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
             "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout", "hdg_condense_adjoint_rhs",
             "hdg_assemble_adjoint", "hdg_backsubstitute_adjoint", "hdg_condense_shifted", "hdg_nnz_counts",
-            "hdg_save_solutions", "hdg_backsubstitute_saved")
+            "hdg_save_solutions", "hdg_backsubstitute_saved", "hdg_skeleton_spmv", "hdg_skeleton_solve")
 
 
 def _ptr(t):
@@ -297,6 +302,23 @@ class Context:
         _f64(B, r_e, lam, u)
         self._check(self._L.hdg_backsubstitute(self._h, *map(_ptr, (factors, B, r_e, lam, u)), _stream(stream)),
                     "hdg_backsubstitute")
+
+    # ---- the skeleton solve: SURVEY.md §8(f) NEXT #3, PAPER.md:357-362 -----------------------------------------------
+    def skeleton_spmv(self, K, x, y, stream=None):
+        """y = K x over the owned rows (x: global trace vector)."""
+        _f64(K, x, y)
+        self._check(self._L.hdg_skeleton_spmv(self._h, _ptr(K), _ptr(x), _ptr(y), _stream(stream)),
+                    "hdg_skeleton_spmv")
+
+    def skeleton_solve(self, K, E, lam, rtol=1e-10, maxit=500, restart=40, stream=None):
+        """K lam = E by block-Jacobi-preconditioned GMRES(restart); lam in: guess, out: solution. Returns
+        (iterations, true relative residual)."""
+        _f64(K, E, lam)
+        it, rr = ctypes.c_int(), ctypes.c_double()
+        self._check(self._L.hdg_skeleton_solve(self._h, _ptr(K), _ptr(E), _ptr(lam), float(rtol), int(maxit),
+                                               int(restart), ctypes.byref(it), ctypes.byref(rr), _stream(stream)),
+                    "hdg_skeleton_solve")
+        return it.value, rr.value
 
     # ---- saved local solutions: SURVEY.md §8(f) NEXT #2, PAPER.md:359 ------------------------------------------------
     def save_solutions(self, factors, B, r_e, X, stream=None):

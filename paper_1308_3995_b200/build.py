@@ -8,7 +8,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libhdg.so")
 SOURCES = ["api.cu", "condense.cu", "condense_sweep.cu", "condense_warp.cu", "backsub.cu", "skeleton.cu", "adjoint.cu",
-           "comm.cu", "condense_rows.cu", "solutions.cu"]
+           "comm.cu", "condense_rows.cu", "solutions.cu",
+           "skeleton_solve.cu"]
 HEADERS = ["hdg_internal.cuh", "dev_common.cuh", os.path.join("..", "..", "include", "hdg.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]

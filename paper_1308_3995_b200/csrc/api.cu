@@ -64,6 +64,8 @@ void free_plan(Plan& p) {
   cudaFree(p.d_scratch);
   cudaFree(p.d_send); cudaFree(p.d_recv);
   cudaFree(p.d_redo); cudaFree(p.d_redo_count); cudaFree(p.d_mark);
+  cudaFree(p.sw.V); cudaFree(p.sw.w); cudaFree(p.sw.z); cudaFree(p.sw.partial); cudaFree(p.sw.h); cudaFree(p.sw.Dinv);
+  cudaFree(p.sw.dinv_off);
   p = Plan();
 }
 
@@ -282,6 +284,7 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     }
   std::vector<int64_t> face_off(F + 1, 0);
   for (int64_t f = 0; f < F; ++f) face_off[f + 1] = face_off[f] + m->face_ndof[f];
+  for (int64_t f = 0; f < F; ++f) p.max_face_ndof = std::max<int>(p.max_face_ndof, m->face_ndof[f]);
   p.n_trace = face_off[F];
 
   std::vector<int32_t> ne(n), nf(n);
@@ -764,6 +767,44 @@ hdg_status hdg_backsubstitute_saved(hdg_ctx ctx, const double* X, const double* 
   return solutions_call(ctx, 1, "hdg_backsubstitute_saved", nullptr, nullptr, nullptr, X, lambda, u, stream);
 }
 
+// ---- §8(f) NEXT #3: the skeleton solve ----------------------------------------------------
+hdg_status hdg_skeleton_spmv(hdg_ctx ctx, const double* K, const double* x, double* y, hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_skeleton_spmv: no plan");
+  ctx->launches = 0;
+  if (p.sk.f1 == p.sk.f0) return HDG_OK;
+  if (!K || !x || !y) return fail(ctx, HDG_ERR_ARG, "hdg_skeleton_spmv: null pointer");
+  if (p.max_face_ndof > 32) return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_skeleton_spmv: face trace size > 32");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  HDG_CUDA(ctx, skeleton_spmv(p, K, x, y, s, &ctx->launches));
+  return HDG_OK;
+}
+
+hdg_status hdg_skeleton_solve(hdg_ctx ctx, const double* K, const double* E, double* lambda, double rtol, int maxit,
+                              int restart, int* iters, double* relres, hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_skeleton_solve: no plan");
+  ctx->launches = 0;
+  if (!iters || !relres) return fail(ctx, HDG_ERR_ARG, "hdg_skeleton_solve: null iters/relres");
+  if (ctx->nranks != 1)
+    return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_skeleton_solve: single rank only (the distributed solve is not built)");
+  if (p.sk.ntr > 0 && (!K || !E || !lambda)) return fail(ctx, HDG_ERR_ARG, "hdg_skeleton_solve: null pointer");
+  if (!(rtol > 0.0) || maxit < 1 || restart < 1 || restart > 200)
+    return fail(ctx, HDG_ERR_ARG, "hdg_skeleton_solve: rtol > 0, maxit >= 1, 1 <= restart <= 200 required");
+  if (p.max_face_ndof > kMaxFaceSolve)
+    return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_skeleton_solve: face trace size %d > %d", p.max_face_ndof, kMaxFaceSolve);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  const cudaError_t e = skeleton_gmres(p, p.sw, K, E, lambda, rtol, maxit, restart, s, iters, relres, &ctx->launches);
+  if (e == cudaErrorMemoryAllocation) return fail(ctx, HDG_ERR_NOMEM, "hdg_skeleton_solve: workspace");
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "hdg_skeleton_solve");
+  return HDG_OK;
+}
+
 }  // extern "C"
+
 
 

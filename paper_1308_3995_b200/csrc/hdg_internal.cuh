@@ -166,6 +166,15 @@ struct Skeleton {
   int64_t* d_recv_items = nullptr;  // [n][3]: face, global element, offset in recv buffer
 };
 
+// skeleton solve workspace (skeleton_solve.cu): Krylov basis, block-Jacobi inverses, reduction partials
+constexpr int kMaxFaceSolve = 24;   // largest face trace size of the skeleton solve (C5: 4 (5 + 1))
+struct SolverWork {
+  int64_t n = -1;
+  int m = 0;
+  double *V = nullptr, *w = nullptr, *z = nullptr, *partial = nullptr, *h = nullptr, *Dinv = nullptr;
+  int64_t* dinv_off = nullptr;
+};
+
 struct Plan {
   bool valid = false;
   int64_t E = 0, F = 0, eb = 0, n = 0;
@@ -178,6 +187,8 @@ struct Plan {
   Skeleton sk;
   double* d_scratch = nullptr;
   int64_t scratch_doubles = 0;
+  SolverWork sw;
+  int max_face_ndof = 0;
   int32_t* d_redo = nullptr;       // [n] + count: the row-tile kernel's redo list, and its per-element marks
   int32_t* d_redo_count = nullptr;
   int32_t* d_mark = nullptr;
@@ -218,6 +229,10 @@ cudaError_t launch_exact_list(const CondenseArgs& a, const int32_t* list, const 
 cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_adjoint(const AdjointArgs& a, int mode, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_save_solutions(const SolutionsArgs& a, int sms, cudaStream_t s, int64_t* launches);
+cudaError_t skeleton_gmres(const Plan& p, SolverWork& sw, const double* K, const double* E, double* x, double rtol,
+                           int maxit, int m, cudaStream_t s, int* iters, double* relres, int64_t* launches);
+cudaError_t skeleton_spmv(const Plan& p, const double* K, const double* x, double* y, cudaStream_t s,
+                          int64_t* launches);
 cudaError_t launch_backsub_saved(const SolutionsArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t skeleton_symbolic(Plan& p, cudaStream_t s);
 cudaError_t launch_assemble(const Plan& p, const double* S, const double* g, double* K, double* E, double* send,
