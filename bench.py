@@ -185,10 +185,19 @@ class ClockSampler:
     def mark(self):
         self.t_mark = time.time()
 
-    def stop(self):
+    def stop(self, replay=None):
+        """replay: a callable re-running the timed step; for regions shorter than nvidia-smi's sampling (C1, C2)
+        it is re-run for ~0.4 s after the timed region while the sampler keeps going, and the clocks are taken
+        from that window (noted in the record)."""
         t_end = time.time()
         if self.proc is None:
             return None
+        if replay is not None and t_end - (self.t_mark or t_end) < 0.3:
+            t0 = time.time()
+            while time.time() - t0 < 0.4:
+                replay()
+            self.t_mark, t_end = t0, time.time()
+            self.replayed = True
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -207,6 +216,9 @@ class ClockSampler:
             return {"samples": 0, "note": "no nvidia-smi sample"}
         inside = [r for r in rows if self.t_mark is not None and self.t_mark - 0.05 <= r[0] <= t_end + 0.05]
         note = None
+        if getattr(self, "replayed", False):
+            note = ("timed region shorter than the 100 ms sampling interval: clocks sampled while the same step "
+                    "re-ran for 0.4 s right after it")
         if not inside:
             inside = rows[-3:]
             note = "timed region shorter than the 100 ms sampling interval: last samples of the warm-up and region"
@@ -659,7 +671,12 @@ def main():
         step(evs[i])
     t1.record(stream)
     torch.cuda.synchronize()
-    clk = clocks.stop()
+
+    def _replay():
+        step()
+        torch.cuda.synchronize()
+
+    clk = clocks.stop(replay=_replay)
     if world > 1:
         dist.barrier()
     total_ms = t0.elapsed_time(t1) if flush is None else sum(e[0].elapsed_time(e[3]) for e in evs)

@@ -57,6 +57,7 @@ struct RowGeo {
 };
 
 struct RowCfg {
+  int D;       // disjoint slots: C rows delayed by D = NS - 1 elements
   int NS;      // U-store slots (elements in flight)
   int P;       // pool doubles
   int ovl;     // overlap mode (NS == 2): row tiles >= ovl of slot s overlap the other slot's region
@@ -227,18 +228,38 @@ __global__ void __launch_bounds__(NWARPS * 32, 1) rows_kernel(const CondenseArgs
     //   A(0) | H(1) C(0) T(1) | H(2) C(1) T(2) | ... | C(n-1)
     // H = A row tiles [0, hr), T = [hr, TA): the rows of an overlapping slot that wait for the previous element
     // (hr = cfg.ovl in overlap mode, else TA).
+    // Disjoint slots (NS >= 2): the C rows are delayed by D = NS - 1 elements, so up to NS elements' chains are
+    // in flight:  A(0) .. A(D-1) | A(D) C(0) | A(D+1) C(1) | ... | C(n-D) .. C(n-1)
+    // (A(p+D) reuses the slot of element p+D-NS < p, whose C rows come earlier).
     int t, tile;
     {
-      const int hr = cfg.overlap ? cfg.ovl : TA, TC = NT - TA;
-      if (q < TA) {
-        t = 0;
-        tile = q;
+      const int TC = NT - TA;
+      if (cfg.overlap) {
+        const int hr = cfg.ovl;
+        if (q < TA) {
+          t = 0;
+          tile = q;
+        } else {
+          const int qq = q - TA, p = qq / NT, r = qq - p * NT;
+          if (p >= n_local - 1) { t = p; tile = TA + r; }              // the last element's C rows
+          else if (r < hr) { t = p + 1; tile = r; }                     // H(p+1)
+          else if (r < hr + TC) { t = p; tile = TA + (r - hr); }        // C(p)
+          else { t = p + 1; tile = r - TC; }                            // T(p+1)
+        }
       } else {
-        const int qq = q - TA, p = qq / NT, r = qq - p * NT;
-        if (p >= n_local - 1) { t = p; tile = TA + r; }              // the last element's C rows
-        else if (r < hr) { t = p + 1; tile = r; }                     // H(p+1)
-        else if (r < hr + TC) { t = p; tile = TA + (r - hr); }        // C(p)
-        else { t = p + 1; tile = r - TC; }                            // T(p+1)
+        const int D = min(cfg.D, n_local), Pm = n_local - D;
+        if (q < D * TA) {
+          t = q / TA;
+          tile = q - t * TA;
+        } else if (q - D * TA < Pm * NT) {
+          const int qq = q - D * TA, p = qq / NT, r = qq - p * NT;
+          if (r < TA) { t = p + D; tile = r; }
+          else { t = p; tile = r; }
+        } else {
+          const int qq = q - D * TA - Pm * NT;
+          t = Pm + qq / TC;
+          tile = TA + qq % TC;
+        }
       }
     }
     const int s = t % cfg.NS;
@@ -276,6 +297,7 @@ __global__ void __launch_bounds__(NWARPS * 32, 1) rows_kernel(const CondenseArgs
       const double* P0 = isA ? a.A + a.offA[l] + (int64_t)rr * ne : a.C + a.offC[l] + (int64_t)rr * ne;
       const double* P1 = isA ? a.B + a.offB[l] + (int64_t)rr * nf : a.D + a.offD[l] + (int64_t)rr * nf;
       const double vlast = real ? __ldg(isA ? a.re + a.offRe[l] + r : a.rf + a.offRf[l] + r) : 0.0;
+      const double shv = (isA && real && a.shift) ? __ldg(a.shift + a.offRe[l] + r) : 0.0;
 #pragma unroll
       for (int j = 0; j < NCTM; ++j) {
         const int c0 = 8 * j + 2 * tig;
@@ -290,9 +312,9 @@ __global__ void __launch_bounds__(NWARPS * 32, 1) rows_kernel(const CondenseArgs
       for (int j = 0; j < NCTM; ++j) {
         const int c0 = 8 * j + 2 * tig;
         if (real && c0 - RA == nf) x[j][0] = vlast;                       // the r_e / r_f column
-        if (isA && real && a.shift) {                                     // re-condensation: A_e + diag(shift_e)
-          if (c0 == r) x[j][0] += __ldg(a.shift + a.offRe[l] + r);
-          if (c0 + 1 == r) x[j][1] += __ldg(a.shift + a.offRe[l] + r);
+        if (j == i) {                                                     // re-condensation: A_e + diag(shift_e)
+          if (c0 == r) x[j][0] += shv;                                    // (the diagonal is in tile i)
+          if (c0 + 1 == r) x[j][1] += shv;
         }
         if (isA && !real) {                                               // identity padding rows of A
           x[j][0] = c0 == r ? 1.0 : 0.0;
@@ -493,8 +515,11 @@ bool rows_config(int ne, int nf, size_t smem_optin, RowCfg* cfg, int64_t* smem_b
     c.P = (int)(c.NS * slot);
     c.overlap = 0;
     c.ovl = G.TA;
+    const char* dv = getenv("HDG_ROWS_DELAY");   // experiments: the C-row delay (1 .. NS - 1)
+    c.D = dv ? std::max(1, std::min(c.NS - 1, atoi(dv))) : 1;   // (C3: D = 1 49.9, 2 49.8, 3 57.8 ms)
   } else {
     c.NS = 2;
+    c.D = 1;
     c.P = (int)avail;
     c.overlap = 1;
     c.ovl = G.TA;
