@@ -550,16 +550,15 @@ def run_step(wl, ev=None):
     n = 0
     if ev:
         ev[0].record(stream)
-    ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], wl["S"], wl["g"], wl["F"], wl["infot"],
-                 stream=stream)
-    n += ctx.launch_count()
     if wl.get("X") is not None:
-        if ev:
-            ev[4].record(stream)
-        ctx.save_solutions(wl["F"], inp["B"], inp["re"], wl["X"], stream=stream)
-        n += ctx.launch_count()
-        if ev:
-            ev[5].record(stream)
+        # §8(f) NEXT #2: the condensation also saves X = A^-1 [B | r_e] (written by the kernels that
+        # form it; a save pass on the fresh factors for the others)
+        ctx.condense_saved(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], wl["S"], wl["g"], wl["F"],
+                           wl["X"], wl["infot"], stream=stream)
+    else:
+        ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], wl["S"], wl["g"], wl["F"],
+                     wl["infot"], stream=stream)
+    n += ctx.launch_count()
     if ev:
         ev[1].record(stream)
     ctx.assemble_skeleton(wl["S"], wl["g"], wl["K"], wl["E"], send=wl["send"], stream=stream)
@@ -683,13 +682,11 @@ def main():
     cond_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     asm_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     bs_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
-    save_ms = (sum(e[4].elapsed_time(e[5]) for e in evs) / args.steps) if args.path == "saved" else 0.0
     gpu_launches = launches[0]
-    t = torch.tensor([total_ms, cond_ms, asm_ms, bs_ms, save_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, cond_ms, asm_ms, bs_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, cond_ms, asm_ms, bs_ms, save_ms = t.tolist()
-    cond_ms -= save_ms       # (ev[1] follows the save in the saved path)
+    total_ms, cond_ms, asm_ms, bs_ms = t.tolist()
     ms_step = total_ms / args.steps
 
     # ---- CUDA graph of G back-to-back steps (no flush between them): separates launch latency
@@ -816,11 +813,12 @@ def main():
             "condense_per_s": elems / (cond_ms * 1e-3), "backsub_per_s": elems / (bs_ms * 1e-3),
             "condense_ms": cond_ms, "assemble_ms": asm_ms, "backsub_ms": bs_ms,
             "backsub_hbm_gbs": work["backsub_bytes"] / (bs_ms * 1e-3) / 1e9,
-            **({"path": "saved", "save_solutions_ms": save_ms,
+            **({"path": "saved",
                 "backsub_saved_bytes": float(sum(8 * int(a) * (int(b) + 1) + 8 * int(b) + 8 * int(a) for a, b in
                                                  zip(w.elem_ne[eb:eb + n], w.elem_nf[eb:eb + n]))),
-                "note": "condense_ms excludes hdg_save_solutions (save_solutions_ms); backsub_ms is the GEMV on "
-                        "the saved X (backsub_saved_bytes: X, lambda_e gather, u)"} if args.path == "saved" else {}),
+                "note": "condense_ms is hdg_condense_saved (X written by the warp/panel kernels, a save pass on "
+                        "the factors for sweep buckets); backsub_ms is the GEMV on the saved X (backsub_saved_bytes: "
+                        "X, lambda_e gather, u)"} if args.path == "saved" else {}),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

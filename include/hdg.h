@@ -201,6 +201,15 @@ hdg_status hdg_backsubstitute(hdg_ctx ctx, const void* factors, const double* B,
 hdg_status hdg_save_solutions(hdg_ctx ctx, const void* factors, const double* B, const double* r_e, double* X,
                               hdg_stream stream);
 
+/* hdg_condense that also saves the local solutions X (as hdg_save_solutions would): the condensation kernels that
+ * form X = A_e^-1 [B_e | r_e] on the way to S_e (the warp-per-element kernel, n_e <= 32, and the panel kernel)
+ * write it from shared memory; for the buckets whose kernels never form it (the sweep kernels eliminate the C rows
+ * alongside A instead) the save pass runs on the fresh factors. Arguments as hdg_condense plus X (device,
+ * plan.len_X doubles). */
+hdg_status hdg_condense_saved(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                              const double* r_e, const double* r_f, double* S, double* g, void* factors, double* X,
+                              int32_t* info, hdg_stream stream);
+
 /* Reconstruction from the saved solutions: u_e = y_e - X_e[:, 0:n_f] lambda_e (= A_e^-1 (r_e - B_e lambda_e)),
  * a GEMV per element reading n_e (n_f + 1) doubles instead of the factors, B_e and r_e. lambda as for
  * hdg_backsubstitute; u packed like hdg_backsubstitute's. */

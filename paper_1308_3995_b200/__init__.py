@@ -77,6 +77,8 @@ def lib():
         L.hdg_condense.argtypes = [P] + [P] * 10 + [P]
         L.hdg_condense_shifted.restype = I32
         L.hdg_condense_shifted.argtypes = [P] + [P] * 11 + [P]
+        L.hdg_condense_saved.restype = I32
+        L.hdg_condense_saved.argtypes = [P] + [P] * 11 + [P]
         L.hdg_save_solutions.restype = I32
         L.hdg_save_solutions.argtypes = [P] + [P] * 4 + [P]
         L.hdg_backsubstitute_saved.restype = I32
@@ -122,7 +124,8 @@ EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status
             "hdg_exchange_counts", "hdg_skeleton_accumulate", "hdg_backsubstitute", "hdg_first_error",
             "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout", "hdg_condense_adjoint_rhs",
             "hdg_assemble_adjoint", "hdg_backsubstitute_adjoint", "hdg_condense_shifted", "hdg_nnz_counts",
-            "hdg_save_solutions", "hdg_backsubstitute_saved", "hdg_skeleton_spmv", "hdg_skeleton_solve")
+            "hdg_save_solutions", "hdg_backsubstitute_saved", "hdg_skeleton_spmv", "hdg_skeleton_solve",
+            "hdg_condense_saved")
 
 
 def _ptr(t):
@@ -321,6 +324,12 @@ class Context:
         return it.value, rr.value
 
     # ---- saved local solutions: SURVEY.md §8(f) NEXT #2, PAPER.md:359 ------------------------------------------------
+    def condense_saved(self, A, B, C, D, r_e, r_f, S, g, factors, X, info, stream=None):
+        """hdg_condense that also saves X_e = A_e^-1 [B_e | r_e] (written by the kernels that form it)."""
+        _f64(A, B, C, D, r_e, r_f, S, g, X)
+        self._check(self._L.hdg_condense_saved(self._h, *map(_ptr, (A, B, C, D, r_e, r_f, S, g, factors, X, info)),
+                                               _stream(stream)), "hdg_condense_saved")
+
     def save_solutions(self, factors, B, r_e, X, stream=None):
         """X_e = A_e^-1 [B_e | r_e] (n_e x (n_f + 1) row-major per element) from the saved factors."""
         _f64(B, r_e, X)

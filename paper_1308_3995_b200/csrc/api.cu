@@ -441,7 +441,8 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
 
 static hdg_status condense_impl(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
                                 const double* r_e, const double* r_f, const double* shift, double* S, double* g,
-                                void* factors, int32_t* info, hdg_stream stream, const char* name) {
+                                void* factors, int32_t* info, hdg_stream stream, const char* name,
+                                double* X = nullptr) {
   if (!ctx) return HDG_ERR_ARG;
   const Plan& p = ctx->plan;
   if (!p.valid) return fail(ctx, HDG_ERR_STATE, "%s: no plan", name);
@@ -451,6 +452,7 @@ static hdg_status condense_impl(hdg_ctx ctx, const double* A, const double* B, c
   for (const void* q : ptrs)
     if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "%s: null or misaligned (16 B) pointer", name);
   if (shift && !aligned16(shift)) return fail(ctx, HDG_ERR_ARG, "%s: misaligned (16 B) shift", name);
+  if (X && !aligned16(X)) return fail(ctx, HDG_ERR_ARG, "%s: misaligned (16 B) X", name);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   HDG_CUDA(ctx, cudaSetDevice(ctx->device));
   for (const Bucket& b : p.buckets) {
@@ -468,11 +470,23 @@ static hdg_status condense_impl(hdg_ctx ctx, const double* A, const double* B, c
     a.trace = ctx->trace;
     a.debug = getenv("HDG_DEBUG_MODE") ? atoi(getenv("HDG_DEBUG_MODE")) : 0;
     a.redo = p.d_redo; a.redo_count = p.d_redo_count; a.mark = p.d_mark;
+    // saved solutions: the warp and panel kernels form X and write it; the others get the save pass from the factors
+    const bool forms_x = b.warp || (!b.rows && !b.sweep && !b.sweep_gt);
+    a.Xout = (X && forms_x) ? X : nullptr;
+    a.offX = p.d_off[OFF_X];
     if (b.warp) HDG_CUDA(ctx, launch_condense_warp(a, ctx->sms, s, &ctx->launches));
     else if (b.rows) HDG_CUDA(ctx, launch_condense_rows(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
     else if (b.sweep) HDG_CUDA(ctx, launch_condense_sweep(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
     else if (b.sweep_gt) HDG_CUDA(ctx, launch_condense_sweep_gt(a, ctx->sms, s, &ctx->launches));
     else HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
+    if (X && !forms_x) {
+      SolutionsArgs q{};
+      q.factors = a.factors; q.B = B; q.re = r_e; q.X = X;
+      q.elems = b.d_elems;
+      q.offB = p.d_off[OFF_B]; q.offRe = p.d_off[OFF_RE]; q.offF = p.d_off[OFF_F]; q.offX = p.d_off[OFF_X];
+      q.ne = b.ne; q.nf = b.nf; q.count = b.count;
+      HDG_CUDA(ctx, launch_save_solutions(q, ctx->sms, s, &ctx->launches));
+    }
   }
   return HDG_OK;
 }
@@ -481,6 +495,13 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
                         const double* r_e, const double* r_f, double* S, double* g, void* factors, int32_t* info,
                         hdg_stream stream) {
   return condense_impl(ctx, A, B, C, D, r_e, r_f, nullptr, S, g, factors, info, stream, "hdg_condense");
+}
+
+hdg_status hdg_condense_saved(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                              const double* r_e, const double* r_f, double* S, double* g, void* factors, double* X,
+                              int32_t* info, hdg_stream stream) {
+  if (ctx && ctx->plan.valid && ctx->plan.n > 0 && !X) return fail(ctx, HDG_ERR_ARG, "hdg_condense_saved: null X");
+  return condense_impl(ctx, A, B, C, D, r_e, r_f, nullptr, S, g, factors, info, stream, "hdg_condense_saved", X);
 }
 
 hdg_status hdg_condense_shifted(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,

@@ -702,6 +702,12 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
       // ---- a3 backward part: X = U^-1 W on columns [CB, C8), panels bottom-up ---------------------------------
       for (int ct = warp; ct < ((C8 - CB) >> 3); ct += NWARPS) backsolve_tile(T, ldT, ne, Uinv_all, CB + ct * 8, lane);
       __syncthreads();
+      if (a.Xout) {   // §8(f) NEXT #2: the local solutions X = A^-1 [B | r_e] are formed here anyway — save them
+        double* Xo = a.Xout + a.offX[l];
+        const int nw = nf + 1;
+        for (int i = warp; i < ne; i += NWARPS)
+          for (int j = lane; j < nw; j += 32) Xo[(int64_t)i * nw + j] = T[i * ldT + CB + j];
+      }
     }
     HDG_STAMP(a.trace, tit, 5);
     // the A columns of T are free from here on: start streaming the next element's A_e

@@ -147,6 +147,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
           if (a1) T[i * kLdT + c1] = fma(-u, x1, T[i * kLdT + c1]);
         }
       }
+      if (a.Xout) {   // §8(f) NEXT #2: the local solutions X = A^-1 [B | r_e] (columns ne .. nc of T) — save them
+        __syncwarp();
+        double* Xo = a.Xout + a.offX[l];
+        for (int i = 0; i < ne; ++i) {
+          if (a0) Xo[(int64_t)i * nw + c0 - ne] = T[i * kLdT + c0];
+          if (a1) Xo[(int64_t)i * nw + c1 - ne] = T[i * kLdT + c1];
+        }
+      }
       // W's padding columns [nc, kLdT) read as zeros by the last X fragment
       if (c0 >= nc)
         for (int i = 0; i < ne; ++i) T[i * kLdT + c0] = 0.0;

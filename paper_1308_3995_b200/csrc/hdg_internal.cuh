@@ -88,6 +88,8 @@ struct CondenseArgs {
   double* scratch;        // global workspace for T when it does not fit in shared memory
   long long* trace;       // instrumentation: clock64 stamps of CTA 0 (NULL = off)
   int debug;              // profiling experiments only (HDG_DEBUG_MODE): 1 = workers skip their MMA work
+  double* Xout;           // NULL, or the saved local solutions X_e = A_e^-1 [B_e | r_e] (n_e x (n_f+1), at offX)
+  const int64_t* offX;
   int32_t* redo;          // row-tile kernel: elements whose GEPP speculation failed (redone on the exact path)
   int32_t* redo_count;
   int32_t* mark;          // [n] per-element failed-speculation marks (zero between calls)

@@ -65,3 +65,29 @@ def test_saved_solutions_gpu(cuda, name, nr, nt):
     torch.cuda.synchronize()
     assert rel_fro_per_element(Xg.cpu().numpy()[:len(X)], X, offX) < 1e-11
     assert rel_fro_per_element(u.cpu().numpy()[:len(us)], us, offU) < 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,nr,nt,kern", [("C2", 4, 8, None), ("C3", 3, 8, None), ("C3", 3, 8, "sweep"),
+                                             ("C4", 3, 6, None), ("C4", 3, 6, "panel"), ("C5", 4, 10, None)])
+def test_condense_saved_fused(cuda, monkeypatch, name, nr, nt, kern):
+    """hdg_condense_saved: X written by the warp / panel kernels during the condensation, by the save pass for the
+    sweep buckets — the same X as the oracle's, and the same S, g as hdg_condense."""
+    import torch
+    import paper_1308_3995_b200 as hdg
+    if kern:
+        monkeypatch.setenv("HDG_CONDENSE_KERNEL", kern)
+    w = gen.config(name, nr=nr, nt=nt)
+    blk = gen.host_blocks(w)
+    lam = gen.host_lambda(w)
+    c, X, offX, us, offU = _uvec_oracle(w, blk, lam)
+    ctx = hdg.Context(0)
+    ctx.plan(w.elem_face, w.face_elem, w.face_ndof, w.elem_ne)
+    d = {k: to_dev(blk[k]) for k in ("A", "B", "C", "D", "re", "rf")}
+    S, g, F, inf, Xg, u = (ctx.alloc(k) for k in ("S", "g", "factors", "info", "X", "u"))
+    ctx.condense_saved(d["A"], d["B"], d["C"], d["D"], d["re"], d["rf"], S, g, F, Xg, inf)
+    ctx.backsubstitute_saved(Xg, to_dev(lam), u)
+    torch.cuda.synchronize()
+    assert rel_fro_per_element(Xg.cpu().numpy()[:len(X)], X, offX) < 1e-11
+    assert rel_fro_per_element(S.cpu().numpy()[:len(c["S"])], c["S"], c["off_S"]) < 1e-11
+    assert rel_fro_per_element(u.cpu().numpy()[:len(us)], us, offU) < 1e-11
