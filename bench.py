@@ -132,8 +132,19 @@ def run_adjoint(args, wl, rank, world, local):
 
 
 def _traffic(key):
+    """DRAM read + write bytes per launch of the dominant kernel from the committed `ncu --set full` capture
+    (profiles/traffic.json), only while the kernel's source is unchanged since that capture (same hash as
+    tools/summarize_profiles.py recorded); otherwise None — a stale figure is never reported."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(key)
+        e = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(key)
+    except Exception:
+        return None
+    if not isinstance(e, dict):
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    try:
+        from summarize_profiles import source_sha
+        return e["bytes"] if source_sha(e.get("kernel", "")) == e.get("source_sha") else None
     except Exception:
         return None
 
@@ -791,11 +802,7 @@ def main():
                     "frac": cond_gbs / (hbm or 6551.4), "traffic": None, "kernel": kname,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6551.4",
                     "bytes_per_launch": work["condense_bytes"], "fp64_tflops": cond_tflops}
-        try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-            roof["traffic"] = tr.get(args.config)
-        except Exception:
-            pass
+        roof["traffic"] = _traffic(args.config)
         line = {
             "metric": METRIC, "value": elems / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

@@ -56,11 +56,34 @@ def launches(path):
     return tot, cnt
 
 
-def raw_metrics(rep):
+def raw_metrics(rep, kernel=None):
+    """Counters of one captured launch: the first one, or the first whose name contains `kernel`."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
-    h, u, v = r[0], r[1], r[2]
-    return {a: (c, b) for a, b, c in zip(h, u, v)}, v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+    h, u = r[0], r[1]
+    ki = h.index("Kernel Name") if "Kernel Name" in h else None
+    v = r[2]
+    if kernel and ki is not None:
+        v = next((row for row in r[2:] if kernel in row[ki]), r[2])
+    return {a: (c, b) for a, b, c in zip(h, u, v)}, v[ki] if ki is not None else "?"
+
+
+# source files whose change makes a stored traffic figure stale (bench.py recomputes the same hash)
+KERNEL_SOURCES = {"sweep_kernel": "condense_sweep.cu", "condense_kernel": "condense.cu", "warp_kernel": "condense_warp.cu",
+                  "adjoint_kernel": "adjoint.cu", "backsub_saved_kernel": "solutions.cu", "save_kernel": "solutions.cu",
+                  "backsub_kernel": "backsub.cu", "rows_kernel": "condense_rows.cu"}
+
+
+def source_sha(kname):
+    import hashlib
+    csrc = os.path.join(ROOT, "paper_1308_3995_b200", "csrc")
+    f = next((v for k, v in KERNEL_SOURCES.items() if k in kname), None)
+    if f is None:
+        return None
+    h = hashlib.sha256()
+    for name in (f, "dev_common.cuh", "hdg_internal.cuh"):
+        h.update(open(os.path.join(csrc, name), "rb").read())
+    return h.hexdigest()[:16]
 
 
 def hot_lines(rep, top=25):
@@ -82,6 +105,7 @@ def main():
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--config", action="append", default=[])
     ap.add_argument("--note", default="")
+    ap.add_argument("--kernel", action="append", default=[], help="per --rep: the captured launch to summarise")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
@@ -104,10 +128,12 @@ def main():
         print("wrote", path)
     tpath = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    for rep, cfg in zip(a.rep, a.config):
-        m, kname = raw_metrics(rep)
+    kernels = a.kernel + [None] * (len(a.rep) - len(a.kernel))
+    for rep, cfg, kf in zip(a.rep, a.config, kernels):
+        m, kname = raw_metrics(rep, kf)
         short = ("condense_sweep" if "sweep_kernel" in kname else "adjoint" if "adjoint" in kname else
-                 "condense" if "condense" in kname else
+                 "condense" if "condense" in kname else "backsub_saved" if "backsub_saved" in kname else
+                 "save_solutions" if "save_kernel" in kname else
                  "backsub" if "backsub" in kname else "".join(ch for ch in kname.split("(")[0][-30:] if ch.isalnum()))
         path = os.path.join(PROF, f"{a.tag}_{short}_{cfg}_ncu.md")
         with open(path, "w") as f:
@@ -117,10 +143,12 @@ def main():
                 if key in m:
                     f.write(f"| {label} (`{key}`) | {m[key][0]} | {m[key][1]} |\n")
             f.write("\nWarp-stall samples by source line (tools/ncu_hot.py):\n\n```\n" + hot_lines(rep) + "```\n")
-        if "dram__bytes_read.sum" in m and short.startswith("condense"):
+        if "dram__bytes_read.sum" in m:
             rd = to_bytes(*m["dram__bytes_read.sum"])
             wr = to_bytes(*m["dram__bytes_write.sum"])
-            traffic[cfg] = rd + wr
+            key = cfg if short.startswith("condense") else f"{cfg}_{short}"
+            traffic[key] = {"bytes": rd + wr, "kernel": kname[:120], "source_sha": source_sha(kname),
+                            "profile": os.path.relpath(path, ROOT)}
         print("wrote", path)
     json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
 
