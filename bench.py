@@ -131,6 +131,79 @@ def run_adjoint(args, wl, rank, world, local):
     return 0
 
 
+def run_solve(args, wl, rank, world, local):
+    """The Newton step with the skeleton solve in it (§8(f) NEXT #3): condense -> assemble -> solve K lambda = E
+    (block-Jacobi GMRES, rtol 1e-10, from lambda = 0) -> back-substitute with the computed lambda. Reports the solve
+    time, its iterations and the SpMV's HBM rate (K's values + column gathers per iteration)."""
+    import torch
+    if world > 1:
+        raise SystemExit("--path solve: single rank (the distributed skeleton solve is not built)")
+    w, ctx, stream, inp = wl["w"], wl["ctx"], wl["stream"], wl["inp"]
+    info = wl["info"]
+    lam = torch.zeros(w.n_trace, dtype=torch.float64, device=torch.device("cuda", local))
+    y = ctx.alloc("E")
+    res = []
+
+    def step(timed):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record(stream)
+        ctx.condense(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], wl["S"], wl["g"], wl["F"],
+                     wl["infot"], stream=stream)
+        ev[1].record(stream)
+        ctx.assemble_skeleton(wl["S"], wl["g"], wl["K"], wl["E"], stream=stream)
+        ev[2].record(stream)
+        lam.zero_()
+        it, rr = ctx.skeleton_solve(wl["K"], wl["E"], lam, rtol=1e-10, maxit=2000, restart=40, stream=stream)
+        ev[3].record(stream)
+        ctx.backsubstitute(wl["F"], inp["B"], inp["re"], lam, wl["u"], stream=stream)
+        ev[4].record(stream)
+        torch.cuda.synchronize()
+        if timed:
+            res.append(([ev[i].elapsed_time(ev[i + 1]) for i in range(4)], it, rr))
+
+    for _ in range(args.warmup):
+        step(False)
+    clocks = ClockSampler(local)
+    clocks.start()
+    clocks.mark()
+    for _ in range(args.steps):
+        step(True)
+    clk = clocks.stop()
+    # one SpMV alone (HBM rate of the solver's dominant kernel)
+    a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x = torch.randn(w.n_trace, dtype=torch.float64, device=lam.device)
+    ctx.skeleton_spmv(wl["K"], x, y, stream=stream)
+    a_.record(stream)
+    for _ in range(10):
+        ctx.skeleton_spmv(wl["K"], x, y, stream=stream)
+    b_.record(stream)
+    torch.cuda.synchronize()
+    spmv_ms = a_.elapsed_time(b_) / 10
+    spmv_bytes = 8.0 * info.nvals + 4.0 * info.nnzb + 8.0 * (info.nnzb + 1) + 16.0 * w.n_trace
+    t = np.array([r[0] for r in res]).mean(axis=0)
+    its = [r[1] for r in res]
+    hbm = measured_peaks().get("hbm_gbs") or 6551.4
+    line = {"metric": "Newton step with the skeleton solve (fp64): condense + assemble + GMRES + back-substitute",
+            "value": w.E / (t.sum() * 1e-3), "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(t.sum()), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "impl": "hdg", "path": "solve",
+            "data": "synthetic (seeded Philox blocks with BASELINE.json distributions, generated in HBM)",
+            "config": {"workload": args.config, "elements": w.E, "trace_dofs": w.n_trace, "nnz_blocks": info.nnzb,
+                       "solver": "GMRES(40), right block-Jacobi, rtol 1e-10, lambda0 = 0"},
+            "condense_ms": float(t[0]), "assemble_ms": float(t[1]), "solve_ms": float(t[2]), "backsub_ms": float(t[3]),
+            "solve_iterations": its, "solve_true_relres": [r[2] for r in res],
+            "solve_ms_per_iteration": float(t[2]) / max(1, np.mean(its)),
+            "spmv_ms": spmv_ms, "spmv_hbm_gbs": spmv_bytes / (spmv_ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "spmv_kernel (skeleton_solve.cu)",
+                         "achieved": spmv_bytes / (spmv_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": spmv_bytes / (spmv_ms * 1e-3) / 1e9 / hbm, "traffic": None,
+                         "bytes_per_launch": spmv_bytes},
+            "clocks": clk, "e2e": None, "cpu_baseline": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def _traffic(key):
     """DRAM read + write bytes per launch of the dominant kernel from the committed `ncu --set full` capture
     (profiles/traffic.json), only while the kernel's source is unchanged since that capture (same hash as
@@ -603,7 +676,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--path", default="primal", choices=["primal", "adjoint", "saved"],
+    ap.add_argument("--path", default="primal", choices=["primal", "adjoint", "saved", "solve"],
                     help="adjoint: time the transposed path (SURVEY.md §8(f) NEXT #1) on the primal factors; saved: "
                          "save the local solutions after the condensation and reconstruct from them (NEXT #2)")
     ap.add_argument("--graph", type=int, default=0,
@@ -638,6 +711,8 @@ def main():
     wl = setup_workload(args.config, rank, world, local, slab=args.slab)
     if args.path == "adjoint":
         return run_adjoint(args, wl, rank, world, local)
+    if args.path == "solve":
+        return run_solve(args, wl, rank, world, local)
     if args.path == "saved":
         wl["X"] = wl["ctx"].alloc("X")
     w, ctx, info, stream, inp, lam = wl["w"], wl["ctx"], wl["info"], wl["stream"], wl["inp"], wl["lam"]
