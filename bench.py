@@ -116,7 +116,8 @@ def run_adjoint(args, wl, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "impl": "hdg", "path": "adjoint",
             "data": "synthetic (seeded Philox blocks; r~_e, lambda~ seeded stand-ins)",
-            "config": {"workload": args.config, "elements": int(n), "n_e": int(ne.max()), "n_f": int(nf.max()),
+            "config": {"workload": args.config + (f" mesh at p = {args.degree}" if args.degree else ""),
+                       "elements": int(n), "n_e": int(ne.max()), "n_f": int(nf.max()),
                        "step": "condense_adjoint_rhs + assemble_adjoint + backsubstitute_adjoint"},
             "adjoint_rhs_ms": rhs_ms, "assemble_adjoint_ms": asm_ms, "backsub_adjoint_ms": bs_ms,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
@@ -410,7 +411,18 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def setup_workload(config: str, rank: int = 0, world: int = 1, local: int = 0, slab=None):
+def workload_of(config: str, degree=None):
+    """The BASELINE config, or its mesh at another uniform polynomial degree (--degree: e.g. the adjoint's
+    enriched degree p + 1)."""
+    import gen
+    if degree is None:
+        return gen.config(config)
+    c = gen.CONFIGS[config]
+    return gen.make_workload(f"{config}-p{degree}", nr=c["nr"], nt=c["nt"], m_elem=c["m_elem"], p_fixed=int(degree),
+                             seed=gen.SEED_BASE + 1 + list(gen.CONFIGS).index(config))
+
+
+def setup_workload(config: str, rank: int = 0, world: int = 1, local: int = 0, slab=None, degree=None):
     """The benchmark's launch configuration (shared with the full-size parity tests): this rank's element slab of
     the BASELINE config, inputs generated directly in HBM (bit-identical to gen.host_blocks), plan built once,
     outputs allocated. slab = (r, P): emulate rank r of a P-way partition on this single GPU (used for C5, whose
@@ -420,7 +432,7 @@ def setup_workload(config: str, rank: int = 0, world: int = 1, local: int = 0, s
     import gen
     import paper_1308_3995_b200 as hdg
     dev = torch.device("cuda", local)
-    w = gen.config(config)
+    w = workload_of(config, degree)
     if slab is not None:
         r_emul, p_emul = slab
         reb = slab_bounds(w.E, p_emul)
@@ -679,6 +691,8 @@ def main():
     ap.add_argument("--path", default="primal", choices=["primal", "adjoint", "saved", "solve"],
                     help="adjoint: time the transposed path (SURVEY.md §8(f) NEXT #1) on the primal factors; saved: "
                          "save the local solutions after the condensation and reconstruct from them (NEXT #2)")
+    ap.add_argument("--degree", type=int, default=None,
+                    help="run the config's mesh at this uniform degree (C1-C4; e.g. the adjoint at p + 1)")
     ap.add_argument("--graph", type=int, default=0,
                     help="also time G back-to-back steps captured in one CUDA graph (launch latency; C1/C2)")
     ap.add_argument("--slab", default=None,
@@ -708,7 +722,7 @@ def main():
     if args.config == "C5" and args.slab is None:
         # C5 (~490 GB of inputs) does not fit one B200: the whole mesh in element slabs, several per GPU
         return run_chunked(args, rank, world, local, dmma_peak)
-    wl = setup_workload(args.config, rank, world, local, slab=args.slab)
+    wl = setup_workload(args.config, rank, world, local, slab=args.slab, degree=args.degree)
     if args.path == "adjoint":
         return run_adjoint(args, wl, rank, world, local)
     if args.path == "solve":

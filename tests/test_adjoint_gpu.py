@@ -183,3 +183,13 @@ def test_adjoint_argument_errors(cuda):
     with pytest.raises(hdg.HDGError) as ei:
         ctx.assemble_adjoint(None, x, x, x)
     assert ei.value.status == hdg.HDG_ERR_ARG
+
+
+@pytest.mark.parametrize("p", [4, 5])
+def test_adjoint_enriched_degree(cuda, p):
+    """The adjoint at the enriched degree p + 1 ("the adjoint is approximated with p+1"): C4's
+    Navier-Stokes mixed blocks at p = 4 (n_e = 180) and 5 (n_e = 252) — the elements larger than one SM, whose
+    primal factors come from the global-slab sweep kernel."""
+    w = gen.make_workload(f"C4-p{p}", nr=2, nt=6, m_elem=12, p_fixed=p, seed=gen.SEED_BASE + 4)
+    assert int(w.elem_ne[0]) == (180 if p == 4 else 252)
+    _adjoint_case(w, gen.host_blocks(w), seed=31 + p)
