@@ -646,6 +646,19 @@ def run_step(wl, ev=None):
     n = 0
     if ev:
         ev[0].record(stream)
+    if wl.get("fused"):
+        # §8(f) NEXT #2: condensation and assembly fused (S_e, g_e straight into K, E; bitwise the same K, E)
+        ctx.condense_assemble(inp["A"], inp["B"], inp["C"], inp["D"], inp["re"], inp["rf"], wl["K"], wl["E"], wl["F"],
+                              wl["infot"], stream=stream)
+        n += ctx.launch_count()
+        if ev:
+            ev[1].record(stream)
+            ev[2].record(stream)
+        ctx.backsubstitute(wl["F"], inp["B"], inp["re"], wl["lam"], wl["u"], stream=stream)
+        n += ctx.launch_count()
+        if ev:
+            ev[3].record(stream)
+        return n
     if wl.get("X") is not None:
         # §8(f) NEXT #2: the condensation also saves X = A^-1 [B | r_e] (written by the kernels that
         # form it; a save pass on the fresh factors for the others)
@@ -688,7 +701,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--path", default="primal", choices=["primal", "adjoint", "saved", "solve"],
+    ap.add_argument("--path", default="primal", choices=["primal", "adjoint", "saved", "solve", "fused"],
                     help="adjoint: time the transposed path (SURVEY.md §8(f) NEXT #1) on the primal factors; saved: "
                          "save the local solutions after the condensation and reconstruct from them (NEXT #2)")
     ap.add_argument("--degree", type=int, default=None,
@@ -729,6 +742,10 @@ def main():
         return run_solve(args, wl, rank, world, local)
     if args.path == "saved":
         wl["X"] = wl["ctx"].alloc("X")
+    if args.path == "fused":
+        if world > 1:
+            raise SystemExit("--path fused: single rank (hdg_condense_assemble)")
+        wl["fused"] = True
     w, ctx, info, stream, inp, lam = wl["w"], wl["ctx"], wl["info"], wl["stream"], wl["inp"], wl["lam"]
     S, g, u, F, infot, K, E, send, recv = (wl[k] for k in ("S", "g", "u", "F", "infot", "K", "E", "send", "recv"))
     eb, n, reb = wl["eb"], wl["n"], wl["reb"]

@@ -144,6 +144,23 @@ hdg_status hdg_condense_shifted(hdg_ctx ctx, const double* A, const double* B, c
                                 const double* r_e, const double* r_f, const double* shift, double* S, double* g,
                                 void* factors, int32_t* info, hdg_stream stream);
 
+/* Fused condensation and assembly (§8(f) NEXT #2): as hdg_condense followed by hdg_assemble_skeleton, but S_e and
+ * g_e never reach HBM — the condensation kernels add them into K and E from their registers / shared memory
+ * (fp64 atomics). Every entry of K and E has at most two contributions (the left and the right element of its
+ * face), and (0 + a) + b == (0 + b) + a in IEEE arithmetic, so K and E are bitwise those of the ordered
+ * left-then-right gather. K [plan.nvals], E [plan.n_owned_trace]: device outputs, zeroed by the call
+ * first; factors and info as for hdg_condense (S and g are not produced: the adjoint assembly needs hdg_condense).
+ * Single rank (HDG_ERR_UNSUPPORTED otherwise: shared-face rows need the exchange). The block-CSR structure of K is
+ * the plan's (hdg_skeleton_structure). */
+hdg_status hdg_condense_assemble(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                                 const double* r_e, const double* r_f, double* K, double* E, void* factors,
+                                 int32_t* info, hdg_stream stream);
+
+/* Copy the plan's block-CSR structure of the owned rows (as hdg_assemble_skeleton does): row_ptr [n_owned_faces+1],
+ * col_idx [nnzb], blk_off [nnzb+1] (device; any may be NULL). Stream-ordered. */
+hdg_status hdg_skeleton_structure(hdg_ctx ctx, int32_t* row_ptr, int32_t* col_idx, int64_t* blk_off,
+                                  hdg_stream stream);
+
 /* a6 (+a7 pack) assembly of the owned skeleton rows: K[f, f'] = sum over local elements e adjacent to both of
  * S_e[slot(f), slot(f')], E[f] = sum of g_e[slot(f)], contributions taken left (lower element id) then right
  * (SURVEY.md S10). Block-CSR over owned rows: row_ptr [n_owned_faces + 1] int32 (block

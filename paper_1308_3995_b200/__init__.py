@@ -77,6 +77,10 @@ def lib():
         L.hdg_condense.argtypes = [P] + [P] * 10 + [P]
         L.hdg_condense_shifted.restype = I32
         L.hdg_condense_shifted.argtypes = [P] + [P] * 11 + [P]
+        L.hdg_condense_assemble.restype = I32
+        L.hdg_condense_assemble.argtypes = [P] + [P] * 10 + [P]
+        L.hdg_skeleton_structure.restype = I32
+        L.hdg_skeleton_structure.argtypes = [P, P, P, P, P]
         L.hdg_condense_saved.restype = I32
         L.hdg_condense_saved.argtypes = [P] + [P] * 11 + [P]
         L.hdg_save_solutions.restype = I32
@@ -125,7 +129,7 @@ EXPORTED = ("hdg_version", "hdg_max_elem_ndof", "hdg_max_face_ndof", "hdg_status
             "hdg_launch_count", "hdg_debug_set_trace", "hdg_exchange_layout", "hdg_condense_adjoint_rhs",
             "hdg_assemble_adjoint", "hdg_backsubstitute_adjoint", "hdg_condense_shifted", "hdg_nnz_counts",
             "hdg_save_solutions", "hdg_backsubstitute_saved", "hdg_skeleton_spmv", "hdg_skeleton_solve",
-            "hdg_condense_saved")
+            "hdg_condense_saved", "hdg_condense_assemble", "hdg_skeleton_structure")
 
 
 def _ptr(t):
@@ -324,6 +328,17 @@ class Context:
         return it.value, rr.value
 
     # ---- saved local solutions: SURVEY.md §8(f) NEXT #2, PAPER.md:359 ------------------------------------------------
+    def condense_assemble(self, A, B, C, D, r_e, r_f, K, E, factors, info, stream=None):
+        """Fused condensation + skeleton assembly (single rank): S_e, g_e go straight into K, E (bitwise equal to
+        condense + assemble_skeleton)."""
+        _f64(A, B, C, D, r_e, r_f, K, E)
+        self._check(self._L.hdg_condense_assemble(self._h, *map(_ptr, (A, B, C, D, r_e, r_f, K, E, factors, info)),
+                                                  _stream(stream)), "hdg_condense_assemble")
+
+    def skeleton_structure(self, row_ptr=None, col_idx=None, blk_off=None, stream=None):
+        self._check(self._L.hdg_skeleton_structure(self._h, *map(_ptr, (row_ptr, col_idx, blk_off)), _stream(stream)),
+                    "hdg_skeleton_structure")
+
     def condense_saved(self, A, B, C, D, r_e, r_f, S, g, factors, X, info, stream=None):
         """hdg_condense that also saves X_e = A_e^-1 [B_e | r_e] (written by the kernels that form it)."""
         _f64(A, B, C, D, r_e, r_f, S, g, X)

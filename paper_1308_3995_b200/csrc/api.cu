@@ -66,6 +66,7 @@ void free_plan(Plan& p) {
   cudaFree(p.d_redo); cudaFree(p.d_redo_count); cudaFree(p.d_mark);
   cudaFree(p.sw.V); cudaFree(p.sw.w); cudaFree(p.sw.z); cudaFree(p.sw.partial); cudaFree(p.sw.h); cudaFree(p.sw.Dinv);
   cudaFree(p.sw.dinv_off);
+  cudaFree(p.d_eblk); cudaFree(p.d_eE); cudaFree(p.d_eslot);
   p = Plan();
 }
 
@@ -439,16 +440,54 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
   return HDG_OK;
 }
 
+// fused condense -> assemble tables (per local element: the K offset of each of its 3 x 3 slot-pair blocks, the E
+// offset of each slot, the slot start rows), built once per plan from the block-CSR structure
+static hdg_status build_fused_tables(hdg_ctx ctx) {
+  Plan& p = ctx->plan;
+  if (p.d_eblk) return HDG_OK;
+  const Skeleton& k = p.sk;
+  const int64_t nrows = k.f1 - k.f0, n = p.n;
+  std::vector<int32_t> rp(nrows + 1), ci(std::max<int64_t>(k.nnzb, 1)), ef(3 * p.E), fnd(p.F);
+  std::vector<int64_t> bo(k.nnzb + 1), fo(p.F + 1);
+  HDG_CUDA(ctx, cudaMemcpy(rp.data(), k.d_row_ptr, sizeof(int32_t) * (nrows + 1), cudaMemcpyDeviceToHost));
+  if (k.nnzb) HDG_CUDA(ctx, cudaMemcpy(ci.data(), k.d_col_idx, sizeof(int32_t) * k.nnzb, cudaMemcpyDeviceToHost));
+  HDG_CUDA(ctx, cudaMemcpy(bo.data(), k.d_blk_off, sizeof(int64_t) * (k.nnzb + 1), cudaMemcpyDeviceToHost));
+  HDG_CUDA(ctx, cudaMemcpy(ef.data(), p.d_elem_face, sizeof(int32_t) * 3 * p.E, cudaMemcpyDeviceToHost));
+  HDG_CUDA(ctx, cudaMemcpy(fnd.data(), p.d_face_ndof, sizeof(int32_t) * p.F, cudaMemcpyDeviceToHost));
+  HDG_CUDA(ctx, cudaMemcpy(fo.data(), p.d_face_off, sizeof(int64_t) * (p.F + 1), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> eblk(9 * std::max<int64_t>(n, 1), -1), eE(3 * std::max<int64_t>(n, 1), -1);
+  std::vector<int32_t> eslot(4 * std::max<int64_t>(n, 1), 0);
+  for (int64_t l = 0; l < n; ++l) {
+    const int32_t* f = ef.data() + 3 * (p.eb + l);
+    int32_t* so = eslot.data() + 4 * l;
+    for (int a = 0; a < 3; ++a) so[a + 1] = so[a] + (f[a] >= 0 ? fnd[f[a]] : 0);
+    for (int a = 0; a < 3; ++a) {
+      if (f[a] < 0 || f[a] < k.f0 || f[a] >= k.f1) continue;   // no trace, or a row owned by another rank
+      eE[3 * l + a] = fo[f[a]] - k.tr0;
+      const int64_t r = f[a] - k.f0;
+      for (int b = 0; b < 3; ++b) {
+        if (f[b] < 0) continue;
+        for (int q = rp[r]; q < rp[r + 1]; ++q)
+          if (ci[q] == f[b]) { eblk[9 * l + 3 * a + b] = bo[q]; break; }
+      }
+    }
+  }
+  HDG_CUDA(ctx, upload(&p.d_eblk, eblk.data(), eblk.size()));
+  HDG_CUDA(ctx, upload(&p.d_eE, eE.data(), eE.size()));
+  HDG_CUDA(ctx, upload(&p.d_eslot, eslot.data(), eslot.size()));
+  return HDG_OK;
+}
+
 static hdg_status condense_impl(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
                                 const double* r_e, const double* r_f, const double* shift, double* S, double* g,
                                 void* factors, int32_t* info, hdg_stream stream, const char* name,
-                                double* X = nullptr) {
+                                double* X = nullptr, double* Kf = nullptr, double* Ef = nullptr) {
   if (!ctx) return HDG_ERR_ARG;
   const Plan& p = ctx->plan;
   if (!p.valid) return fail(ctx, HDG_ERR_STATE, "%s: no plan", name);
   ctx->launches = 0;
   if (p.n == 0) return HDG_OK;
-  const void* ptrs[] = {A, B, C, D, r_e, r_f, S, g, factors, info};
+  const void* ptrs[] = {A, B, C, D, r_e, r_f, Kf ? (const void*)Kf : S, Kf ? (const void*)Ef : g, factors, info};
   for (const void* q : ptrs)
     if (!q || !aligned16(q)) return fail(ctx, HDG_ERR_ARG, "%s: null or misaligned (16 B) pointer", name);
   if (shift && !aligned16(shift)) return fail(ctx, HDG_ERR_ARG, "%s: misaligned (16 B) shift", name);
@@ -459,6 +498,7 @@ static hdg_status condense_impl(hdg_ctx ctx, const double* A, const double* B, c
     CondenseArgs a;
     a.A = A; a.B = B; a.C = C; a.D = D; a.re = r_e; a.rf = r_f; a.S = S; a.g = g;
     a.shift = shift;
+    a.Kf = Kf; a.Ef = Ef; a.eblk = p.d_eblk; a.eE = p.d_eE; a.eslot = p.d_eslot;
     a.factors = static_cast<unsigned char*>(factors);
     a.info = info;
     a.elems = b.d_elems;
@@ -495,6 +535,40 @@ hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const dou
                         const double* r_e, const double* r_f, double* S, double* g, void* factors, int32_t* info,
                         hdg_stream stream) {
   return condense_impl(ctx, A, B, C, D, r_e, r_f, nullptr, S, g, factors, info, stream, "hdg_condense");
+}
+
+hdg_status hdg_condense_assemble(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
+                                 const double* r_e, const double* r_f, double* K, double* E, void* factors,
+                                 int32_t* info, hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_condense_assemble: no plan");
+  if (ctx->nranks != 1)
+    return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_condense_assemble: single rank (shared-face rows need the exchange)");
+  if ((p.sk.nvals > 0 && !K) || (p.sk.ntr > 0 && !E)) return fail(ctx, HDG_ERR_ARG, "hdg_condense_assemble: null K/E");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  const hdg_status st = build_fused_tables(ctx);
+  if (st != HDG_OK) return st;
+  if (p.sk.nvals > 0) HDG_CUDA(ctx, cudaMemsetAsync(K, 0, sizeof(double) * p.sk.nvals, s));
+  if (p.sk.ntr > 0) HDG_CUDA(ctx, cudaMemsetAsync(E, 0, sizeof(double) * p.sk.ntr, s));
+  if (p.n == 0) return HDG_OK;
+  return condense_impl(ctx, A, B, C, D, r_e, r_f, nullptr, nullptr, nullptr, factors, info, stream,
+                       "hdg_condense_assemble", nullptr, K, E);
+}
+
+hdg_status hdg_skeleton_structure(hdg_ctx ctx, int32_t* row_ptr, int32_t* col_idx, int64_t* blk_off,
+                                  hdg_stream stream) {
+  if (!ctx) return HDG_ERR_ARG;
+  const Plan& p = ctx->plan;
+  if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_skeleton_structure: no plan");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  HDG_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int64_t nrows = p.sk.f1 - p.sk.f0;
+  if (row_ptr) HDG_CUDA(ctx, cudaMemcpyAsync(row_ptr, p.sk.d_row_ptr, sizeof(int32_t) * (nrows + 1), cudaMemcpyDeviceToDevice, s));
+  if (col_idx && p.sk.nnzb) HDG_CUDA(ctx, cudaMemcpyAsync(col_idx, p.sk.d_col_idx, sizeof(int32_t) * p.sk.nnzb, cudaMemcpyDeviceToDevice, s));
+  if (blk_off) HDG_CUDA(ctx, cudaMemcpyAsync(blk_off, p.sk.d_blk_off, sizeof(int64_t) * (p.sk.nnzb + 1), cudaMemcpyDeviceToDevice, s));
+  return HDG_OK;
 }
 
 hdg_status hdg_condense_saved(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,

@@ -512,9 +512,9 @@ constexpr int kBatchK = 16;   // k4-steps of C_e fragments loaded ahead in phase
 // Phase B work: NI work items (8-row tile of [S | g] x chunk of kChunkCT column tiles) per warp at a time; all
 // their D / r_f / C loads are issued before the first DMMA and the NI independent accumulator sets interleave.
 template <int NI, int NWARPS>
-__device__ __forceinline__ void schur_items(const double* T, int ldT, int ne, int nf, int CB, int CTs, int nchunk,
-                                            const double* Cm, const double* D, const double* rf, double* S, double* g,
-                                            int warp, int lane) {
+__device__ __forceinline__ void schur_items(const SgDst& dst, const double* T, int ldT, int ne, int nf,
+                                            int CB, int CTs, int nchunk, const double* Cm, const double* D,
+                                            const double* rf, int warp, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
   const int nItems = ((nf + 7) >> 3) * nchunk;
   for (int w0 = warp; w0 < nItems; w0 += NI * NWARPS) {
@@ -571,8 +571,8 @@ __device__ __forceinline__ void schur_items(const double* T, int ldT, int ne, in
         for (int j = 0; j < kChunkCT; ++j) {
           const int c = 8 * (j0[i] + j) + 2 * tig;
           if (j0[i] + j < CTs) {
-            if (c < nf) *reinterpret_cast<double2*>(S + (int64_t)row[i] * nf + c) = make_double2(acc[i][j][0], acc[i][j][1]);
-            else if (c == nf) g[row[i]] = acc[i][j][0];
+            if (c < nf) out_S2(dst, nf, row[i], c, acc[i][j][0], acc[i][j][1]);
+            else if (c == nf) out_g(dst, row[i], acc[i][j][0]);
           }
         }
       }
@@ -688,11 +688,11 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
       if (tid == 0) a.info[l] = fail;
     }
 
-    double* S = a.S + a.offS[l];
-    double* g = a.g + a.offG[l];
     if (fail) {
-      for (int i = tid; i < nf * nf; i += THREADS) S[i] = __longlong_as_double(0x7ff8000000000000LL);
-      for (int i = tid; i < nf; i += THREADS) g[i] = __longlong_as_double(0x7ff8000000000000LL);
+      const double nan = __longlong_as_double(0x7ff8000000000000LL);
+      const SgDst dst = sg_dst(a, l);
+      for (int i = tid; i < nf * nf; i += THREADS) out_S1(dst, nf, i / nf, i % nf, nan);
+      for (int i = tid; i < nf; i += THREADS) out_g(dst, i, nan);
       __syncthreads();
       if (T_SMEM)   // NaNs may have reached the padding: restore the zeros
         for (int i = tid; i < geo.t_doubles(); i += THREADS) T[i] = 0.0;
@@ -718,15 +718,16 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
 
     // ---- a4 Schur complement: [S | g] = [D | r_f] - C X, one warp per 8-row tile, DMMA over k = n_e ----------
     if (!fail) {
+      const SgDst dst = sg_dst(a, l);
       const double* Cm = a.C + a.offC[l];
       const double* D = a.D + a.offD[l];
       const double* rf = a.rf + a.offRf[l];
       const int RTs = (nf + 7) >> 3, CTs = (C8 - CB) >> 3;
       const int nchunk = (CTs + kChunkCT - 1) / kChunkCT;
       if (RTs * nchunk > NWARPS)
-        schur_items<2, NWARPS>(T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, S, g, warp, lane);
+        schur_items<2, NWARPS>(dst, T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, warp, lane);
       else
-        schur_items<1, NWARPS>(T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, S, g, warp, lane);
+        schur_items<1, NWARPS>(dst, T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, warp, lane);
     }
     HDG_STAMP(a.trace, tit, 6);
     __syncthreads();

@@ -452,14 +452,13 @@ __global__ void __launch_bounds__(NWARPS * 32, 1) rows_kernel(const CondenseArgs
       }
     } else {
       // ---- C row tile: its [D | r_f] columns now hold [S_e | g_e]
-      double* S = a.S + a.offS[l];
-      double* g = a.g + a.offG[l];
+      const SgDst dst = sg_dst(a, l);
 #pragma unroll
       for (int j = 0; j < NCTM; ++j)
         if (j >= TA && j < nct && rreal) {
           const int c0 = 8 * (j - TA) + 2 * tig;
-          if (c0 < nf) *reinterpret_cast<double2*>(S + (int64_t)rowg * nf + c0) = make_double2(x[j][0], x[j][1]);
-          else if (c0 == nf) g[rowg] = x[j][0];
+          if (c0 < nf) out_S2(dst, nf, rowg, c0, x[j][0], x[j][1]);
+          else if (c0 == nf) out_g(dst, rowg, x[j][0]);
         }
     }
 

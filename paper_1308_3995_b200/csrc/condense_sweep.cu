@@ -540,10 +540,13 @@ __device__ void sweep_pivot(double* T, double* Cr, const SweepGeo& G, const doub
 // TMA loads of the next element that are already in flight into shared memory are left alone). Not inlined:
 // both roles call it.
 template <int THREADS>
-__device__ __noinline__ void exact_element(const double* A, const double* Bm, const double* re, const double* Cm,
-                                           const double* D, const double* rf, const double* sh, double* S, double* g,
-                                           double* LU, int32_t* info, int ne, int nf, double* X, int* piv, int* sfail,
-                                           int tid) {
+__device__ __noinline__ void exact_element(double* S_, double* g_, double* Kf, double* Ef, const int64_t* eblk,
+                                           const int64_t* eE, const int32_t* so, const double* A, const double* Bm,
+                                           const double* re, const double* Cm, const double* D, const double* rf,
+                                           const double* sh, double* LU, int32_t* info, int ne, int nf, double* X,
+                                           int* piv, int* sfail, int tid) {
+  SgDst dst;
+  dst.S = S_; dst.g = g_; dst.Kf = Kf; dst.Ef = Ef; dst.eblk = eblk; dst.eE = eE; dst.so = so;
   const SweepGeo G(ne, nf);
   const int ldT = G.ldT, ldC = G.ldC, CB = G.CB;
   double* T = X;
@@ -552,16 +555,17 @@ __device__ __noinline__ void exact_element(const double* A, const double* Bm, co
   sweep_pivot<THREADS>(T, Cr, G, A, Bm, re, Cm, sh, piv, sfail, tid);
   const int fail = *sfail;
   if (fail) {
-    for (int i = tid; i < nf * nf; i += THREADS) S[i] = __longlong_as_double(0x7ff8000000000000LL);
-    for (int i = tid; i < nf; i += THREADS) g[i] = __longlong_as_double(0x7ff8000000000000LL);
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    for (int i = tid; i < nf * nf; i += THREADS) out_S1(dst, nf, i / nf, i % nf, nan);
+    for (int i = tid; i < nf; i += THREADS) out_g(dst, i, nan);
   } else {
     // [S | g] = [D | r_f] - Y W, ascending k
     for (int idx = tid; idx < nf * (nf + 1); idx += THREADS) {
       const int i = idx / (nf + 1), j = idx - i * (nf + 1);
       double sum = j < nf ? D[(size_t)i * nf + j] : rf[i];
       for (int k = 0; k < ne; ++k) sum = fma(-Cr[(size_t)i * ldC + k], T[(size_t)k * ldT + CB + j], sum);
-      if (j < nf) S[(size_t)i * nf + j] = sum;
-      else g[i] = sum;
+      if (j < nf) out_S1(dst, nf, i, j, sum);
+      else out_g(dst, i, sum);
     }
   }
   for (int idx = tid; idx < ne * ne; idx += THREADS) LU[idx] = T[(size_t)(idx / ne) * ldT + idx % ne];
@@ -593,7 +597,7 @@ __device__ __noinline__ void exact_element(const double* A, const double* Bm, co
 // shared memory — for elements whose working set exceeds one SM (C5's n_e = 180, 252 buckets). The element's rows
 // are then copied in by all threads at its start (no TMA pipeline, no early prologue); everything else is the same
 // code on generic pointers.
-template <int NWARPS, int MAXT, int MINB, bool GT>
+template <int NWARPS, int MAXT, int MINB, bool GT, bool FUSED>
 __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const CondenseArgs a) {
   constexpr int THREADS = NWARPS * 32;
   constexpr int CW = NWARPS - 1;   // the chain warp: the highest warp id wins issue arbitration in its SMSP
@@ -769,11 +773,14 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       if (aborted) {
         ++pc;   // the aborted panel's buffer may be half-written
         __syncthreads();   // A: remaining loads of the next element issued by the loader warp
-        exact_element<THREADS>(a.A + a.offA[l], a.B + a.offB[l], a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l],
-                                a.rf + a.offRf[l], a.shift ? a.shift + a.offRe[l] : nullptr, a.S + a.offS[l],
-                                a.g + a.offG[l],
-                                reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, ne, nf, X, piv, sfail,
-                                tid);
+        {
+          const SgDst d = sg_dst(a, l);
+          exact_element<THREADS>(d.S, d.g, d.Kf, d.Ef, d.eblk, d.eE, d.so, a.A + a.offA[l], a.B + a.offB[l],
+                                 a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l], a.rf + a.offRf[l],
+                                 a.shift ? a.shift + a.offRe[l] : nullptr,
+                                 reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, ne, nf, X, piv, sfail,
+                                 tid);
+        }
       } else {
         SW_STAMP(tit, 6);
         __syncthreads();   // E: every read of T / Cr of this element is done
@@ -951,24 +958,37 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           load_C(ln);
         }
         __syncthreads();   // A
-        exact_element<THREADS>(a.A + a.offA[l], a.B + a.offB[l], a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l],
-                                a.rf + a.offRf[l], a.shift ? a.shift + a.offRe[l] : nullptr, a.S + a.offS[l],
-                                a.g + a.offG[l],
-                                reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, ne, nf, X, piv, sfail,
-                                tid);
+        {
+          const SgDst d = sg_dst(a, l);
+          exact_element<THREADS>(d.S, d.g, d.Kf, d.Ef, d.eblk, d.eE, d.so, a.A + a.offA[l], a.B + a.offB[l],
+                                 a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l], a.rf + a.offRf[l],
+                                 a.shift ? a.shift + a.offRe[l] : nullptr,
+                                 reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, ne, nf, X, piv, sfail,
+                                 tid);
+        }
       } else {
         if (helper) {
           int32_t* perm = reinterpret_cast<int32_t*>(LU + (size_t)ne * ne);
           for (int i = lane; i < ne; i += 32) perm[i] = i;
           if (lane == 0) a.info[l] = 0;
         } else {
-          double* S = a.S + a.offS[l];
-          double* g = a.g + a.offG[l];
+          if constexpr (FUSED) {   // hdg_condense_assemble: straight into K, E
+            const SgDst dst = sg_dst(a, l);
 #pragma unroll
-          for (int s = 0; s < MAXT; ++s) {
-            const int o = offD[s];
-            if (o >= 0) *reinterpret_cast<double2*>(S + o) = make_double2(acc[s][0], acc[s][1]);
-            else if (o < -1) g[-o - 2] = acc[s][0];
+            for (int s = 0; s < MAXT; ++s) {
+              const int o = offD[s];
+              if (o >= 0) out_S2(dst, nf, o / nf, o - (o / nf) * nf, acc[s][0], acc[s][1]);
+              else if (o < -1) out_g(dst, -o - 2, acc[s][0]);
+            }
+          } else {
+            double* S = a.S + a.offS[l];
+            double* g = a.g + a.offG[l];
+#pragma unroll
+            for (int s = 0; s < MAXT; ++s) {
+              const int o = offD[s];
+              if (o >= 0) *reinterpret_cast<double2*>(S + o) = make_double2(acc[s][0], acc[s][1]);
+              else if (o < -1) g[-o - 2] = acc[s][0];
+            }
           }
         }
         SW_STAMP(tit, 6);
@@ -992,7 +1012,7 @@ template <int NWARPS, int MAXT, int MINB, bool GT>
 cudaError_t launch_sweep_t(const CondenseArgs& a, int sms, cudaStream_t s) {
   const SweepGeo G(a.ne, a.nf);
   const int64_t smem = GT ? G.smem_bytes() - 8 * ((int64_t)G.RA * G.ldT + (int64_t)G.NF8 * G.ldC) : G.smem_bytes();
-  auto kern = sweep_kernel<NWARPS, MAXT, MINB, GT>;
+  auto kern = a.Kf ? sweep_kernel<NWARPS, MAXT, MINB, GT, true> : sweep_kernel<NWARPS, MAXT, MINB, GT, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -1026,9 +1046,10 @@ __global__ void __launch_bounds__(THREADS) exact_list_kernel(const CondenseArgs 
   const int n = *count;
   for (int q = blockIdx.x; q < n; q += gridDim.x) {
     const int64_t l = list[q];
-    exact_element<THREADS>(a.A + a.offA[l], a.B + a.offB[l], a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l],
-                           a.rf + a.offRf[l], a.shift ? a.shift + a.offRe[l] : nullptr, a.S + a.offS[l],
-                           a.g + a.offG[l],
+    const SgDst d = sg_dst(a, l);
+    exact_element<THREADS>(d.S, d.g, d.Kf, d.Ef, d.eblk, d.eE, d.so, a.A + a.offA[l], a.B + a.offB[l],
+                           a.re + a.offRe[l], a.C + a.offC[l], a.D + a.offD[l], a.rf + a.offRf[l],
+                           a.shift ? a.shift + a.offRe[l] : nullptr,
                            reinterpret_cast<double*>(a.factors + a.offF[l]), a.info + l, a.ne, a.nf, X, piv, sfail,
                            threadIdx.x);
   }

@@ -23,7 +23,7 @@ constexpr int kWarpsPerCta = 4;
 constexpr int kLdT = 68;       // row stride of T (>= 64 columns; = 4 mod 16: conflict-free DMMA fragment loads)
 constexpr int kMaxTiles = 5;   // 8-wide column tiles of [S | g] (n_f + 1 <= 40)
 
-template <int NE>
+template <int NE, bool FUSED>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseArgs a) {
   extern __shared__ __align__(16) double wsm[];
   const int lane = threadIdx.x & 31;
@@ -126,10 +126,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
     if (lane < ne) perm[lane] = prow;
     if (lane == 0) a.info[l] = fail;
     if (fail) {
-      double* S = a.S + a.offS[l];
-      double* g = a.g + a.offG[l];
-      for (int i = lane; i < nf * nf; i += 32) S[i] = __longlong_as_double(0x7ff8000000000000LL);
-      for (int i = lane; i < nf; i += 32) g[i] = __longlong_as_double(0x7ff8000000000000LL);
+      const double nan = __longlong_as_double(0x7ff8000000000000LL);
+      const SgDst dst = sg_dst(a, l);
+      for (int i = lane; i < nf * nf; i += 32) out_S1(dst, nf, i / nf, i % nf, nan);
+      for (int i = lane; i < nf; i += 32) out_g(dst, i, nan);
       __syncwarp();
       continue;
     }
@@ -164,10 +164,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
     __syncwarp();
     // ---- [S | g] = [D | r_f] - C X on DMMA: 8 x 8 tiles, k over n_e (X = columns ne.. of T) --------------------------
     const double* Cm = a.C + a.offC[l];
+    const SgDst dst = FUSED ? sg_dst(a, l) : SgDst{};
     const double* D = a.D + a.offD[l];
     const double* rf = a.rf + a.offRf[l];
-    double* S = a.S + a.offS[l];
-    double* g = a.g + a.offG[l];
     const double* X = T + ne;
     const int RT = (nf + 7) >> 3, CT = (nw + 7) >> 3;
     for (int rt = 0; rt < RT; ++rt) {
@@ -195,13 +194,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
         for (int kk = 0; kk < NE / 4; ++kk)
           if (4 * kk < ne) dmma(acc, af[kk], (4 * kk + tig < ne) ? X[(4 * kk + tig) * kLdT + ct * 8 + gid] : 0.0);
         if (rv) {
-          if (c + 1 < nf) {
-            *reinterpret_cast<double2*>(S + (int64_t)row * nf + c) = make_double2(acc[0], acc[1]);
-          } else if (c + 1 == nf) {   // odd n_f: the pair straddles S's last column and g
-            S[(int64_t)row * nf + c] = acc[0];
-            g[row] = acc[1];
-          } else if (c == nf) {
-            g[row] = acc[0];
+          if constexpr (FUSED) {   // hdg_condense_assemble: straight into K, E
+            if (c + 1 < nf) {
+              out_S2(dst, nf, row, c, acc[0], acc[1]);
+            } else if (c + 1 == nf) {   // odd n_f: the pair straddles S's last column and g
+              out_S1(dst, nf, row, c, acc[0]);
+              out_g(dst, row, acc[1]);
+            } else if (c == nf) {
+              out_g(dst, row, acc[0]);
+            }
+          } else {
+            double* S = a.S + a.offS[l];
+            double* g = a.g + a.offG[l];
+            if (c + 1 < nf) {
+              *reinterpret_cast<double2*>(S + (int64_t)row * nf + c) = make_double2(acc[0], acc[1]);
+            } else if (c + 1 == nf) {
+              S[(int64_t)row * nf + c] = acc[0];
+              g[row] = acc[1];
+            } else if (c == nf) {
+              g[row] = acc[0];
+            }
           }
         }
       }
@@ -213,17 +225,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
 template <int NE>
 cudaError_t launch_w(const CondenseArgs& a, int sms, cudaStream_t s) {
   const size_t smem = sizeof(double) * kWarpsPerCta * NE * kLdT;
-  cudaError_t e = cudaFuncSetAttribute(warp_kernel<NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = a.Kf ? warp_kernel<NE, true> : warp_kernel<NE, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, warp_kernel<NE>, kWarpsPerCta * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerCta * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int64_t grid = (int64_t)sms * per_sm;
   const int64_t need = (a.count + kWarpsPerCta - 1) / kWarpsPerCta;
   if (grid > need) grid = need;
   grid = grid_cap(grid);
-  warp_kernel<NE><<<(unsigned)grid, kWarpsPerCta * 32, smem, s>>>(a);
+  kern<<<(unsigned)grid, kWarpsPerCta * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
 

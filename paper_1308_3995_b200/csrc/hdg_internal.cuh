@@ -88,12 +88,84 @@ struct CondenseArgs {
   double* scratch;        // global workspace for T when it does not fit in shared memory
   long long* trace;       // instrumentation: clock64 stamps of CTA 0 (NULL = off)
   int debug;              // profiling experiments only (HDG_DEBUG_MODE): 1 = workers skip their MMA work
+  // fused condense -> assemble (hdg_condense_assemble, §8(f) NEXT #2): when Kf != NULL, S_e and g_e go straight
+  // into K and E by fp64 atomics instead of being stored — every K / E entry has at most two contributions (left
+  // and right element of a face) and (0 + a) + b = (0 + b) + a in IEEE arithmetic, so the result is bitwise the
+  // ordered gather's (left then right, R9)
+  double* Kf;
+  double* Ef;
+  const int64_t* eblk;    // [n][9] K offset of block (slot a, slot b) of local element l (-1: row not owned)
+  const int64_t* eE;      // [n][3] E offset of slot a's first dof (-1: not owned)
+  const int32_t* eslot;   // [n][4] slot start rows in S_e: 0, n0, n0 + n1, n_f
   double* Xout;           // NULL, or the saved local solutions X_e = A_e^-1 [B_e | r_e] (n_e x (n_f+1), at offX)
   const int64_t* offX;
   int32_t* redo;          // row-tile kernel: elements whose GEPP speculation failed (redone on the exact path)
   int32_t* redo_count;
   int32_t* mark;          // [n] per-element failed-speculation marks (zero between calls)
 };
+
+// S_e / g_e output of a condensation kernel for one element: stored at S, g, or (fused mode, Kf != NULL) scattered
+// into K / E through the element's block-offset table
+struct SgDst {
+  double* S;             // S_e (NULL in the fused mode)
+  double* g;
+  double* Kf;
+  double* Ef;
+  const int64_t* eblk;   // [9] this element's block offsets in K (-1: row not owned)
+  const int64_t* eE;     // [3]
+  const int32_t* so;     // [4] slot start rows
+};
+__device__ __forceinline__ SgDst sg_dst(const CondenseArgs& a, int64_t l) {
+  SgDst d;
+  d.Kf = a.Kf;
+  d.Ef = a.Ef;
+  if (a.Kf) {
+    d.S = nullptr;
+    d.g = nullptr;
+    d.eblk = a.eblk + 9 * l;
+    d.eE = a.eE + 3 * l;
+    d.so = a.eslot + 4 * l;
+  } else {
+    d.S = a.S + a.offS[l];
+    d.g = a.g + a.offG[l];
+    d.eblk = nullptr;
+    d.eE = nullptr;
+    d.so = nullptr;
+  }
+  return d;
+}
+__device__ __forceinline__ int fused_slot(const int32_t* so, int r) { return r >= so[1] ? (r >= so[2] ? 2 : 1) : 0; }
+// S_e[row][c .. c+1] (c even: both in one face slot, face trace sizes are even)
+__device__ __forceinline__ void out_S2(const SgDst& d, int nf, int row, int c, double v0, double v1) {
+  if (!d.Kf) {
+    *reinterpret_cast<double2*>(d.S + (int64_t)row * nf + c) = make_double2(v0, v1);
+    return;
+  }
+  const int sa = fused_slot(d.so, row), sb = fused_slot(d.so, c);
+  const int64_t base = d.eblk[3 * sa + sb];
+  if (base < 0) return;
+  double* q = d.Kf + base + (int64_t)(row - d.so[sa]) * (d.so[sb + 1] - d.so[sb]) + (c - d.so[sb]);
+  atomicAdd(q, v0);
+  atomicAdd(q + 1, v1);
+}
+__device__ __forceinline__ void out_S1(const SgDst& d, int nf, int row, int c, double v) {
+  if (!d.Kf) {
+    d.S[(int64_t)row * nf + c] = v;
+    return;
+  }
+  const int sa = fused_slot(d.so, row), sb = fused_slot(d.so, c);
+  const int64_t base = d.eblk[3 * sa + sb];
+  if (base >= 0) atomicAdd(d.Kf + base + (int64_t)(row - d.so[sa]) * (d.so[sb + 1] - d.so[sb]) + (c - d.so[sb]), v);
+}
+__device__ __forceinline__ void out_g(const SgDst& d, int row, double v) {
+  if (!d.Kf) {
+    d.g[row] = v;
+    return;
+  }
+  const int sa = fused_slot(d.so, row);
+  const int64_t base = d.eE[sa];
+  if (base >= 0) atomicAdd(d.Ef + base + (row - d.so[sa]), v);
+}
 
 struct BacksubArgs {
   const unsigned char* factors;
@@ -191,6 +263,9 @@ struct Plan {
   int64_t scratch_doubles = 0;
   SolverWork sw;
   int max_face_ndof = 0;
+  int64_t* d_eblk = nullptr;   // fused condense -> assemble tables (built on first use)
+  int64_t* d_eE = nullptr;
+  int32_t* d_eslot = nullptr;
   int32_t* d_redo = nullptr;       // [n] + count: the row-tile kernel's redo list, and its per-element marks
   int32_t* d_redo_count = nullptr;
   int32_t* d_mark = nullptr;
