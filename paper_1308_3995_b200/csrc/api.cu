@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <tuple>
 
 #include "hdg_internal.cuh"
@@ -66,6 +67,7 @@ void free_plan(Plan& p) {
   cudaFree(p.d_redo); cudaFree(p.d_redo_count); cudaFree(p.d_mark);
   cudaFree(p.sw.V); cudaFree(p.sw.w); cudaFree(p.sw.z); cudaFree(p.sw.partial); cudaFree(p.sw.h); cudaFree(p.sw.Dinv);
   cudaFree(p.sw.dinv_off);
+  cudaFree(p.sw.xfull); cudaFree(p.sw.hsend); cudaFree(p.sw.hrecv); cudaFree(p.sw.d_hsend_idx); cudaFree(p.sw.d_hrecv_idx);
   cudaFree(p.d_eblk); cudaFree(p.d_eE); cudaFree(p.d_eslot);
   p = Plan();
 }
@@ -412,6 +414,52 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     p.sk.n_recv_items = (int64_t)x.recv_items.size() / 3;
     HDG_CUDA(ctx, upload(&p.sk.d_send_items, x.send_items.data(), x.send_items.size()));
     HDG_CUDA(ctx, upload(&p.sk.d_recv_items, x.recv_items.data(), x.recv_items.size()));
+    // ---- halo lists of the distributed skeleton solve: the columns of my owned rows owned elsewhere (received
+    //      before every SpMV), and my owned faces in the rows of others (sent); the adjacency is symmetric (two
+    //      faces couple iff they share an element), so both lists follow from my rows alone
+    {
+      auto rank_of = [&](int64_t e) {
+        return (int)(std::upper_bound(m->rank_elem_begin, m->rank_elem_begin + R + 1, e) - m->rank_elem_begin) - 1;
+      };
+      std::vector<int> fown(F);
+      p.rank_tr0.assign(R, 0);
+      p.rank_ntr.assign(R, 0);
+      std::vector<int64_t> fmin_r(R, F), fmax_r(R, -1);
+      for (int64_t f = 0; f < F; ++f) {
+        fown[f] = rank_of(m->face_elem[2 * f]);
+        fmin_r[fown[f]] = std::min(fmin_r[fown[f]], f);
+        fmax_r[fown[f]] = std::max(fmax_r[fown[f]], f);
+      }
+      for (int r = 0; r < R; ++r)
+        if (fmax_r[r] >= 0) {
+          p.rank_tr0[r] = face_off[fmin_r[r]];
+          p.rank_ntr[r] = face_off[fmax_r[r] + 1] - face_off[fmin_r[r]];
+        }
+      std::vector<std::set<int32_t>> sendf(R), recvf(R);
+      for (int64_t f = p.sk.f0; f < p.sk.f1; ++f)
+        for (int side = 0; side < 2; ++side) {
+          const int32_t e = m->face_elem[2 * f + side];
+          if (e < 0) continue;
+          for (int kk = 0; kk < 3; ++kk) {
+            const int32_t c = m->elem_face[3 * e + kk];
+            if (c < 0 || fown[c] == ctx->rank) continue;
+            recvf[fown[c]].insert(c);
+            sendf[fown[c]].insert((int32_t)f);
+          }
+        }
+      p.halo_scnt.assign(R, 0); p.halo_sdsp.assign(R, 0); p.halo_rcnt.assign(R, 0); p.halo_rdsp.assign(R, 0);
+      p.halo_send_idx.clear(); p.halo_recv_idx.clear();
+      for (int r = 0; r < R; ++r) {
+        p.halo_sdsp[r] = (int64_t)p.halo_send_idx.size();
+        for (int32_t f : sendf[r])
+          for (int64_t d = face_off[f]; d < face_off[f + 1]; ++d) p.halo_send_idx.push_back(d);
+        p.halo_scnt[r] = (int64_t)p.halo_send_idx.size() - p.halo_sdsp[r];
+        p.halo_rdsp[r] = (int64_t)p.halo_recv_idx.size();
+        for (int32_t f : recvf[r])
+          for (int64_t d = face_off[f]; d < face_off[f + 1]; ++d) p.halo_recv_idx.push_back(d);
+        p.halo_rcnt[r] = (int64_t)p.halo_recv_idx.size() - p.halo_rdsp[r];
+      }
+    }
     if (ctx->nccl_comm) {   // the library owns the exchange buffers (a7 runs inside hdg_assemble_*)
       if (cudaMalloc(&p.d_send, sizeof(double) * std::max<int64_t>(1, x.send_doubles)) != cudaSuccess ||
           cudaMalloc(&p.d_recv, sizeof(double) * std::max<int64_t>(1, x.recv_doubles)) != cudaSuccess)
@@ -884,8 +932,8 @@ hdg_status hdg_skeleton_solve(hdg_ctx ctx, const double* K, const double* E, dou
   if (!p.valid) return fail(ctx, HDG_ERR_STATE, "hdg_skeleton_solve: no plan");
   ctx->launches = 0;
   if (!iters || !relres) return fail(ctx, HDG_ERR_ARG, "hdg_skeleton_solve: null iters/relres");
-  if (ctx->nranks != 1)
-    return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_skeleton_solve: single rank only (the distributed solve is not built)");
+  if (ctx->nranks != 1 && !ctx->nccl_comm)
+    return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_skeleton_solve: nranks > 1 needs a context with an NCCL communicator");
   if (p.sk.ntr > 0 && (!K || !E || !lambda)) return fail(ctx, HDG_ERR_ARG, "hdg_skeleton_solve: null pointer");
   if (!(rtol > 0.0) || maxit < 1 || restart < 1 || restart > 200)
     return fail(ctx, HDG_ERR_ARG, "hdg_skeleton_solve: rtol > 0, maxit >= 1, 1 <= restart <= 200 required");
@@ -893,7 +941,10 @@ hdg_status hdg_skeleton_solve(hdg_ctx ctx, const double* K, const double* E, dou
     return fail(ctx, HDG_ERR_UNSUPPORTED, "hdg_skeleton_solve: face trace size %d > %d", p.max_face_ndof, kMaxFaceSolve);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   HDG_CUDA(ctx, cudaSetDevice(ctx->device));
-  const cudaError_t e = skeleton_gmres(p, p.sw, K, E, lambda, rtol, maxit, restart, s, iters, relres, &ctx->launches);
+  std::string cerr;
+  const cudaError_t e = skeleton_gmres(p, p.sw, K, E, lambda, rtol, maxit, restart, s, iters, relres, &ctx->launches,
+                                       ctx->nranks > 1 ? ctx->nccl_comm : nullptr, ctx->rank, ctx->nranks, &cerr);
+  if (!cerr.empty()) return fail(ctx, HDG_ERR_NCCL, "hdg_skeleton_solve: %s", cerr.c_str());
   if (e == cudaErrorMemoryAllocation) return fail(ctx, HDG_ERR_NOMEM, "hdg_skeleton_solve: workspace");
   if (e != cudaSuccess) return cuda_fail(ctx, e, "hdg_skeleton_solve");
   return HDG_OK;

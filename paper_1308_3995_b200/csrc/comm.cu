@@ -12,6 +12,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include <nccl.h>
 
@@ -30,6 +31,8 @@ struct NcclApi {
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclGetErrorString) errorString = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
   std::string err;
 };
 
@@ -61,6 +64,8 @@ NcclApi& api() {
     HDG_SYM(groupStart, "ncclGroupStart");
     HDG_SYM(groupEnd, "ncclGroupEnd");
     HDG_SYM(errorString, "ncclGetErrorString");
+    HDG_SYM(allReduce, "ncclAllReduce");
+    HDG_SYM(broadcast, "ncclBroadcast");
 #undef HDG_SYM
   });
   return a;
@@ -127,6 +132,52 @@ bool nccl_exchange(void* comm, const Plan& p, int rank, int nranks, const double
   const ncclResult_t r2 = a.groupEnd();
   if (r != ncclSuccess) { if (err) *err = nccl_msg("ncclSend/ncclRecv", r); return false; }
   if (r2 != ncclSuccess) { if (err) *err = nccl_msg("ncclGroupEnd", r2); return false; }
+  return true;
+}
+
+// sum over ranks, in place, on stream s (the distributed skeleton solve's dot products)
+bool nccl_allreduce_sum(void* comm, double* buf, size_t n, cudaStream_t s, std::string* err) {
+  const ncclResult_t r = api().allReduce(buf, buf, n, ncclFloat64, ncclSum, static_cast<ncclComm_t>(comm), s);
+  if (r != ncclSuccess) {
+    if (err) *err = nccl_msg("ncclAllReduce", r);
+    return false;
+  }
+  return true;
+}
+
+// every rank's segment [off[r], off[r] + cnt[r]) of buf from rank r to all (one group of broadcasts, in place)
+bool nccl_allgatherv_inplace(void* comm, int nranks, const std::vector<int64_t>& off, const std::vector<int64_t>& cnt,
+                             double* buf, cudaStream_t s, std::string* err) {
+  NcclApi& a = api();
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  ncclResult_t r = a.groupStart();
+  for (int q = 0; q < nranks && r == ncclSuccess; ++q)
+    if (cnt[q] > 0) r = a.broadcast(buf + off[q], buf + off[q], (size_t)cnt[q], ncclFloat64, q, c, s);
+  const ncclResult_t r2 = a.groupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess) {
+    if (err) *err = nccl_msg("ncclBroadcast", r != ncclSuccess ? r : r2);
+    return false;
+  }
+  return true;
+}
+
+// grouped point-to-point exchange of per-peer segments: send[peer] (count, offset) from sbuf, recv[peer] into rbuf
+bool nccl_p2p(void* comm, int rank, int nranks, const std::vector<int64_t>& scnt, const std::vector<int64_t>& sdsp,
+              const double* sbuf, const std::vector<int64_t>& rcnt, const std::vector<int64_t>& rdsp, double* rbuf,
+              cudaStream_t s, std::string* err) {
+  NcclApi& a = api();
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  ncclResult_t r = a.groupStart();
+  for (int q = 0; q < nranks && r == ncclSuccess; ++q) {
+    if (q == rank) continue;
+    if (rcnt[q] > 0) r = a.recv(rbuf + rdsp[q], (size_t)rcnt[q], ncclFloat64, q, c, s);
+    if (r == ncclSuccess && scnt[q] > 0) r = a.send(sbuf + sdsp[q], (size_t)scnt[q], ncclFloat64, q, c, s);
+  }
+  const ncclResult_t r2 = a.groupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess) {
+    if (err) *err = nccl_msg("ncclSend/ncclRecv (halo)", r != ncclSuccess ? r : r2);
+    return false;
+  }
   return true;
 }
 

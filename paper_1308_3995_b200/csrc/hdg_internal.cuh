@@ -247,6 +247,14 @@ struct SolverWork {
   int m = 0;
   double *V = nullptr, *w = nullptr, *z = nullptr, *partial = nullptr, *h = nullptr, *Dinv = nullptr;
   int64_t* dinv_off = nullptr;
+  // distributed solve (nranks > 1): the full-length work vector (owned dofs + halo), and the halo exchange lists
+  // (trace-dof indices to send / receive per peer, grouped by peer, faces ascending)
+  double* xfull = nullptr;
+  double *hsend = nullptr, *hrecv = nullptr;
+  int64_t *d_hsend_idx = nullptr, *d_hrecv_idx = nullptr;
+  int64_t n_hsend = 0, n_hrecv = 0;
+  std::vector<int64_t> hs_cnt, hs_dsp, hr_cnt, hr_dsp;
+  bool halo_built = false;
 };
 
 struct Plan {
@@ -263,6 +271,10 @@ struct Plan {
   int64_t scratch_doubles = 0;
   SolverWork sw;
   int max_face_ndof = 0;
+  // distributed skeleton solve (nranks > 1): trace-dof ranges owned by every rank, and the halo lists of this rank
+  // (trace-dof indices sent to / received from each peer, grouped by peer)
+  std::vector<int64_t> rank_tr0, rank_ntr;
+  std::vector<int64_t> halo_send_idx, halo_recv_idx, halo_scnt, halo_sdsp, halo_rcnt, halo_rdsp;
   int64_t* d_eblk = nullptr;   // fused condense -> assemble tables (built on first use)
   int64_t* d_eE = nullptr;
   int32_t* d_eslot = nullptr;
@@ -307,7 +319,8 @@ cudaError_t launch_backsub(const BacksubArgs& a, int sms, cudaStream_t s, int64_
 cudaError_t launch_adjoint(const AdjointArgs& a, int mode, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t launch_save_solutions(const SolutionsArgs& a, int sms, cudaStream_t s, int64_t* launches);
 cudaError_t skeleton_gmres(const Plan& p, SolverWork& sw, const double* K, const double* E, double* x, double rtol,
-                           int maxit, int m, cudaStream_t s, int* iters, double* relres, int64_t* launches);
+                           int maxit, int m, cudaStream_t s, int* iters, double* relres, int64_t* launches,
+                           void* comm = nullptr, int rank = 0, int nranks = 1, std::string* comm_err = nullptr);
 cudaError_t skeleton_spmv(const Plan& p, const double* K, const double* x, double* y, cudaStream_t s,
                           int64_t* launches);
 cudaError_t launch_backsub_saved(const SolutionsArgs& a, int sms, cudaStream_t s, int64_t* launches);
@@ -324,4 +337,10 @@ bool nccl_comm_init(void** comm, int nranks, int rank, const unsigned char* id, 
 void nccl_comm_destroy(void* comm);
 bool nccl_exchange(void* comm, const Plan& p, int rank, int nranks, const double* send, double* recv, cudaStream_t s,
                    std::string* err);
+bool nccl_allreduce_sum(void* comm, double* buf, size_t n, cudaStream_t s, std::string* err);
+bool nccl_allgatherv_inplace(void* comm, int nranks, const std::vector<int64_t>& off, const std::vector<int64_t>& cnt,
+                             double* buf, cudaStream_t s, std::string* err);
+bool nccl_p2p(void* comm, int rank, int nranks, const std::vector<int64_t>& scnt, const std::vector<int64_t>& sdsp,
+              const double* sbuf, const std::vector<int64_t>& rcnt, const std::vector<int64_t>& rdsp, double* rbuf,
+              cudaStream_t s, std::string* err);
 }  // namespace hdg

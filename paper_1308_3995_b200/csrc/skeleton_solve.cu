@@ -21,14 +21,17 @@ namespace {
 constexpr int kRedBlocks = 296;   // 2 x 148 SMs: the fixed partition of every reduction
 constexpr int kRedThreads = 256;
 
-// y[rows of owned face f] = sum over the blocks of row f of K_block * x[cols] (one warp per block row; lane r owns
-// row r of the block row, n_fp <= 32)
+// y[rows of owned face f] = sum over the blocks of row f of K_block * x[cols]. RPW block rows per warp (RPW = 2 when
+// every face has <= 16 trace dofs: half-warps, no idle lanes on C4's 16-dof faces); lane r of a (half-)warp owns
+// row r of its block row.
+template <int RPW>
 __global__ void __launch_bounds__(256) spmv_kernel(const double* K, const double* x, double* y, const int32_t* row_ptr,
                                                    const int32_t* col_idx, const int64_t* blk_off,
                                                    const int32_t* face_ndof, const int64_t* face_off, int64_t f0,
                                                    int64_t nrows, int64_t tr0) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  constexpr int W = 32 / RPW;
+  const int lane = threadIdx.x & (W - 1);
+  const int64_t r = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * RPW + ((threadIdx.x & 31) / W);
   if (r >= nrows) return;
   const int64_t f = f0 + r;
   const int nr = face_ndof[f];
@@ -178,15 +181,27 @@ __global__ void __launch_bounds__(256) axpby_kernel(double alpha, const double* 
   if (i < n) y[i] = alpha * x[i] + beta * y[i];
 }
 
+// halo exchange of the distributed solve: gather the sent trace dofs, scatter the received ones
+__global__ void __launch_bounds__(256) gather_kernel(const double* x, const int64_t* idx, int64_t n, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = x[idx[i]];
+}
+__global__ void __launch_bounds__(256) scatter_kernel(const double* in, const int64_t* idx, int64_t n, double* x) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[idx[i]] = in[i];
+}
+
 unsigned nb(int64_t n, int t) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
 }  // namespace
 
 // The solver (host loop over the kernels above). Single rank: x (global trace vector) is the whole unknown.
 cudaError_t skeleton_gmres(const Plan& p, SolverWork& sw, const double* K, const double* E, double* x, double rtol,
-                           int maxit, int m, cudaStream_t s, int* iters, double* relres, int64_t* launches) {
+                           int maxit, int m, cudaStream_t s, int* iters, double* relres, int64_t* launches,
+                           void* comm, int rank, int nranks, std::string* comm_err) {
   const Skeleton& k = p.sk;
   const int64_t n = k.ntr, nrows = k.f1 - k.f0;
+  const bool dist = comm != nullptr && nranks > 1;
   cudaError_t e;
   // ---- workspace (kept in the plan across solves)
   if (sw.n != n || sw.m != m) {
@@ -208,18 +223,59 @@ cudaError_t skeleton_gmres(const Plan& p, SolverWork& sw, const double* K, const
     sw.n = n;
     sw.m = m;
   }
+  if (dist && !sw.halo_built) {
+    sw.n_hsend = (int64_t)p.halo_send_idx.size();
+    sw.n_hrecv = (int64_t)p.halo_recv_idx.size();
+    if ((e = cudaMalloc(&sw.xfull, sizeof(double) * std::max<int64_t>(p.n_trace, 1))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&sw.hsend, sizeof(double) * std::max<int64_t>(sw.n_hsend, 1))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&sw.hrecv, sizeof(double) * std::max<int64_t>(sw.n_hrecv, 1))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&sw.d_hsend_idx, sizeof(int64_t) * std::max<int64_t>(sw.n_hsend, 1))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&sw.d_hrecv_idx, sizeof(int64_t) * std::max<int64_t>(sw.n_hrecv, 1))) != cudaSuccess) return e;
+    if (sw.n_hsend && (e = cudaMemcpy(sw.d_hsend_idx, p.halo_send_idx.data(), sizeof(int64_t) * sw.n_hsend,
+                                      cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    if (sw.n_hrecv && (e = cudaMemcpy(sw.d_hrecv_idx, p.halo_recv_idx.data(), sizeof(int64_t) * sw.n_hrecv,
+                                      cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    sw.halo_built = true;
+  }
   *iters = 0;
   *relres = 0.0;
-  if (n == 0) return cudaSuccess;
+  // (a rank without owned rows still takes part in every collective below)
+  if (n == 0 && !dist) return cudaSuccess;
+  bool comm_ok = true;
+  // the halo of a full-length vector: my owned dofs that others' rows read, then theirs into mine
+  auto halo = [&](double* xf) {
+    if (!dist || !comm_ok) return;
+    if (sw.n_hsend) gather_kernel<<<nb(sw.n_hsend, 256), 256, 0, s>>>(xf, sw.d_hsend_idx, sw.n_hsend, sw.hsend);
+    comm_ok = nccl_p2p(comm, rank, nranks, p.halo_scnt, p.halo_sdsp, sw.hsend, p.halo_rcnt, p.halo_rdsp, sw.hrecv, s,
+                       comm_err);
+    if (sw.n_hrecv) scatter_kernel<<<nb(sw.n_hrecv, 256), 256, 0, s>>>(sw.hrecv, sw.d_hrecv_idx, sw.n_hrecv, xf);
+    *launches += 2;
+  };
   const int64_t ldv = n;
   double* V = sw.V;
   const int32_t* rp = k.d_row_ptr;
   auto spmv = [&](const double* xin, double* y) {
-    spmv_kernel<<<nb(nrows, 8), 256, 0, s>>>(K, xin, y, rp, k.d_col_idx, k.d_blk_off, p.d_face_ndof, p.d_face_off,
-                                              k.f0, nrows, k.tr0);
+    if (nrows == 0) return;
+    if (p.max_face_ndof <= 16)
+      spmv_kernel<2><<<nb(nrows, 16), 256, 0, s>>>(K, xin, y, rp, k.d_col_idx, k.d_blk_off, p.d_face_ndof,
+                                                   p.d_face_off, k.f0, nrows, k.tr0);
+    else
+      spmv_kernel<1><<<nb(nrows, 8), 256, 0, s>>>(K, xin, y, rp, k.d_col_idx, k.d_blk_off, p.d_face_ndof,
+                                                   p.d_face_off, k.f0, nrows, k.tr0);
     ++*launches;
   };
+  // K v for an owned-length vector v: v into the full-length work vector, its halo, then the SpMV
+  auto spmv_v = [&](const double* v, double* y) {
+    if (!dist) {
+      spmv(v, y);
+      return;
+    }
+    if (n) cudaMemcpyAsync(sw.xfull + k.tr0, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    halo(sw.xfull);
+    spmv(sw.xfull, y);
+  };
   auto prec = [&](const double* in, double* out) {
+    if (nrows == 0) return;
     bjacobi_apply_kernel<<<nb(nrows, 8), 256, 0, s>>>(sw.Dinv, in, out, p.d_face_ndof, p.d_face_off, sw.dinv_off,
                                                       k.f0, nrows, k.tr0);
     ++*launches;
@@ -230,26 +286,32 @@ cudaError_t skeleton_gmres(const Plan& p, SolverWork& sw, const double* K, const
     dots_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(Vb, ldv, kk, w, n, sw.partial);
     dots_final_kernel<<<nb(kk, 64), 64, 0, s>>>(sw.partial, kk, kRedBlocks, sw.h);
     *launches += 2;
+    if (dist && comm_ok) comm_ok = nccl_allreduce_sum(comm, sw.h, (size_t)kk, s, comm_err);   // sum over slabs
+    if (!comm_ok) return cudaErrorUnknown;
     cudaError_t er = cudaMemcpyAsync(host, sw.h, sizeof(double) * kk, cudaMemcpyDeviceToHost, s);
     if (er == cudaSuccess) er = cudaStreamSynchronize(s);
     return er;
   };
-  bjacobi_setup_kernel<<<nb(nrows, 4), 128, 0, s>>>(K, sw.Dinv, rp, k.d_col_idx, k.d_blk_off, p.d_face_ndof,
-                                                    sw.dinv_off, k.f0, nrows);
-  ++*launches;
+  if (nrows > 0) {
+    bjacobi_setup_kernel<<<nb(nrows, 4), 128, 0, s>>>(K, sw.Dinv, rp, k.d_col_idx, k.d_blk_off, p.d_face_ndof,
+                                                      sw.dinv_off, k.f0, nrows);
+    ++*launches;
+  }
+  double* xo = x + k.tr0;   // this rank's owned part of lambda (the whole vector on one rank)
   // ||E||
   double bn = 0.0;
   if ((e = dots(E, 1, E, &bn)) != cudaSuccess) return e;
   bn = std::sqrt(bn);
   if (bn == 0.0) {
-    cudaMemsetAsync(x, 0, sizeof(double) * n, s);
+    cudaMemsetAsync(x, 0, sizeof(double) * p.n_trace, s);
     return cudaStreamSynchronize(s);
   }
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
   int total = 0;
   double res = 0.0;
   while (total < maxit) {
-    // r = E - K x  -> V_0
+    // r = E - K x  -> V_0 (x: the caller's full-length lambda; its halo refreshed first)
+    halo(x);
     spmv(x, sw.w);
     axpby_kernel<<<nb(n, 256), 256, 0, s>>>(1.0, E, -1.0, sw.w, n);
     ++*launches;
@@ -265,7 +327,7 @@ cudaError_t skeleton_gmres(const Plan& p, SolverWork& sw, const double* K, const
     int j = 0;
     for (; j < m && total < maxit; ++j, ++total) {
       prec(V + (int64_t)j * ldv, sw.z);
-      spmv(sw.z, sw.w);
+      spmv_v(sw.z, sw.w);
       // classical Gram-Schmidt, twice (re-orthogonalisation)
       if ((e = dots(V, j + 1, sw.w, hh.data())) != cudaSuccess) return e;
       for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hh[i];
@@ -309,11 +371,14 @@ cudaError_t skeleton_gmres(const Plan& p, SolverWork& sw, const double* K, const
     if ((e = cudaMemcpyAsync(sw.h, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
     combine_kernel<<<nb(n, 256), 256, 0, s>>>(V, ldv, j, sw.h, sw.w, n, false);
     prec(sw.w, sw.z);
-    axpby_kernel<<<nb(n, 256), 256, 0, s>>>(1.0, sw.z, 1.0, x, n);
+    axpby_kernel<<<nb(n, 256), 256, 0, s>>>(1.0, sw.z, 1.0, xo, n);
     *launches += 2;
     if (res <= rtol) break;
   }
-  // the true residual of the returned x
+  // every rank's owned segment to all ranks (lambda replicated, as the back-substitution reads it), then the true
+  // residual of the returned x
+  if (dist && comm_ok) comm_ok = nccl_allgatherv_inplace(comm, nranks, p.rank_tr0, p.rank_ntr, x, s, comm_err);
+  if (!comm_ok) return cudaErrorUnknown;
   spmv(x, sw.w);
   axpby_kernel<<<nb(n, 256), 256, 0, s>>>(1.0, E, -1.0, sw.w, n);
   ++*launches;
@@ -329,8 +394,12 @@ cudaError_t skeleton_spmv(const Plan& p, const double* K, const double* x, doubl
   const Skeleton& k = p.sk;
   const int64_t nrows = k.f1 - k.f0;
   if (nrows <= 0) return cudaSuccess;
-  spmv_kernel<<<nb(nrows, 8), 256, 0, s>>>(K, x, y, k.d_row_ptr, k.d_col_idx, k.d_blk_off, p.d_face_ndof, p.d_face_off,
-                                           k.f0, nrows, k.tr0);
+  if (p.max_face_ndof <= 16)
+    spmv_kernel<2><<<nb(nrows, 16), 256, 0, s>>>(K, x, y, k.d_row_ptr, k.d_col_idx, k.d_blk_off, p.d_face_ndof,
+                                                 p.d_face_off, k.f0, nrows, k.tr0);
+  else
+    spmv_kernel<1><<<nb(nrows, 8), 256, 0, s>>>(K, x, y, k.d_row_ptr, k.d_col_idx, k.d_blk_off, p.d_face_ndof,
+                                                 p.d_face_off, k.f0, nrows, k.tr0);
   ++*launches;
   return cudaGetLastError();
 }

@@ -59,6 +59,21 @@ def main(out_path):
                         np.linalg.norm(ref["K"][bo[q]:bo[q + 1]]) for q in range(len(bo) - 1))
             if worst > 1e-12:
                 msgs.append(f"{name}: K vs oracle {worst:.2e}")
+        # the distributed skeleton solve (§8(f) NEXT #3): GMRES over the slabs (halo exchange before every SpMV,
+        # all-reduced dots), lambda replicated on return; the reconstruction on each slab with it
+        lam = torch.zeros(w.n_trace, dtype=torch.float64, device=dev)
+        it, rr = ctx.skeleton_solve(K, E, lam, rtol=1e-12, maxit=3000, restart=60, stream=stream)
+        stream.synchronize()
+        if rr > 1e-11:
+            msgs.append(f"{name}: rank {rank} distributed solve relres {rr:.2e} after {it}")
+        lams = [None] * world
+        dist.all_gather_object(lams, lam.cpu().numpy())
+        if rank == 0:
+            ref_lam = oracle.pipeline(w, blk=blk)["lam"]            # the O5 dense solve of the whole mesh
+            for q in range(world):
+                err = np.linalg.norm(lams[q] - ref_lam) / np.linalg.norm(ref_lam)
+                if err > 1e-9:
+                    msgs.append(f"{name}: P={world} lambda on rank {q} vs the dense oracle {err:.2e}")
         ctx.close()
         dist.barrier()
     if rank == 0:

@@ -1,7 +1,9 @@
 """T5: the multi-GPU path for real — torchrun, one process per GPU, NCCL over NVLink, the exchange
 INSIDE libhdg (hdg_get_unique_id -> hdg_ctx_create with the id -> hdg_assemble_skeleton packs, runs one grouped
 ncclSend/ncclRecv on the caller's stream and accumulates, no host sync). P12: the concatenated owned rows of K and
-E at P = 2 (and 4, 8 when the GPUs exist) are bit-identical to the single-rank assembly, and match the oracle.
+E at P = 2 (and 4, 8 when the GPUs exist) are bit-identical to the single-rank assembly, and match the oracle; the
+distributed skeleton solve (GMRES over the slabs: NCCL halo exchange before every SpMV, all-reduced dots) returns the
+same lambda on every rank, within 1e-9 of the oracle's dense solve of the whole mesh.
 Skipped when fewer than 2 GPUs are visible (the round's GPU box has one; the driver's multi-GPU box runs it)."""
 import os
 import subprocess
