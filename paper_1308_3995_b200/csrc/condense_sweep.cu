@@ -687,6 +687,10 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     prefetch_l2(a.B + a.offB[l], (uint32_t)(ne * nf * 8));
     prefetch_l2(a.C + a.offC[l], (uint32_t)(nf * ne * 8));
     prefetch_l2(a.D + a.offD[l], (uint32_t)(nf * nf * 8));
+    // r_e / r_f too: the helper's r_e column and the workers' r_f accumulators are the element's first loads
+    // (16-byte granularity: the packed r_e / r_f of an element start 16-byte aligned when n_e, n_f are even)
+    if ((a.offRe[l] & 1) == 0) prefetch_l2(a.re + a.offRe[l], (uint32_t)(((ne + 1) & ~1) * 8));
+    if ((a.offRf[l] & 1) == 0) prefetch_l2(a.rf + a.offRf[l], (uint32_t)(((nf + 1) & ~1) * 8));
   };
 
   if (!GT && blockIdx.x < a.count && warp == 0) {
@@ -729,6 +733,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
             if (a.shift) shift_rows(l, 0, r1);   // the chain warp's first diagonal block: its rows' shift
           }
         } else {
+          if (p == 0) SW_STAMP(tit, 110);
           if (__syncthreads_or(viol)) { aborted = true; break; }
           SW_STAMP(tit, 8 + 4 * p);
           viol = false;
@@ -823,9 +828,19 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         __syncthreads();   // G
       }
       if (helper) {
-        if (lane == 0 && ln >= 0) prefetch(ln);
+        // (the next element's L2 prefetch is issued at panel 1, behind the TMA row copies: issued here, right after
+        // the previous element's last row / C-row copies, it held the helper ~8 K cycles at the first barrier)
+        if (GT && lane == 0 && ln >= 0) prefetch(ln);
+        // the r_e column: every load issued before the first shared store (the generic T pointer could alias the
+        // global input as far as the compiler knows: interleaved load/store pairs serialise on the HBM latency —
+        // measured, the helper reached the first panel barrier 3-6 K cycles after the workers)
         const double* re = a.re + a.offRe[l];
-        for (int i = lane; i < ne; i += 32) T[(size_t)i * ldT + CB + nf] = __ldg(re + i);
+        double rv[(kMaxNe + 31) / 32];
+#pragma unroll
+        for (int q = 0; q < (kMaxNe + 31) / 32; ++q) rv[q] = lane + 32 * q < ne ? __ldg(re + lane + 32 * q) : 0.0;
+#pragma unroll
+        for (int q = 0; q < (kMaxNe + 31) / 32; ++q)
+          if (lane + 32 * q < ne) T[(size_t)(lane + 32 * q) * ldT + CB + nf] = rv[q];
       } else {
         // the accumulators from D_e / r_f (precomputed offsets: no divisions, no branches around the loads)
         const double* D = a.D + a.offD[l];
@@ -849,6 +864,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       bool aborted = false;
       int p_ab = G.npan;
       for (int p = 0; p < G.npan; ++p, ++pc) {
+        if (p == 0) SW_STAMP(tit, 110);
+        if (helper && p == 0 && a.trace && blockIdx.x == 0 && tit < 4 && lane == 0) a.trace[tit * 256 + 112] = clock64();
         if (__syncthreads_or(viol)) { aborted = true; p_ab = p; break; }
         SW_STAMP(tit, 8 + 4 * p);
         viol = false;
@@ -857,6 +874,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           if (p == 1) expect_all();
           fence_proxy_async();
           load_rows(ln, (p - 1) * NB, p * NB);
+          if (p == 1 && lane == 0) prefetch(ln);
         }
         // one panel step; NBC = 16: a full panel, every size below is a compile-time constant (no guards around
         // the fragment loads, so they are scheduled ahead of the DMMAs); NBC = 0: the partial last panel

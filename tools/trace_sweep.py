@@ -44,3 +44,4 @@ for it in (1, 2):
                   f"{lbl[2]} {q[3] - q[2]:6d}")
             prev = q[3]
         print(f"   after loop +{s[100] - prev}  ->E {s[6] - s[100]}  E wait {s[7] - s[6]}  ->end {s[101] - s[7]}")
+        print(f"   reached the first panel barrier at +{s[110] - b}" + (f" (helper warp: +{t[it, 0, 112] - t[it, 1, 0]})" if wp == 1 else ""))
