@@ -618,6 +618,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
   double* Uinv_b = Linv_b + 2 * NB * LDI;          // [2][NB * LDI]
   double* bcast = Uinv_b + 2 * NB * LDI;           // [2][BCW] (spare)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(bcast + 2 * BCW);   // [0] A rows < 16, [1] everything else
+  // work-claim counters in the two spare barrier slots: [0..1] trailing blocks, [2..3] TRSM jobs (panel parity)
+  int* qctr = reinterpret_cast<int*>(mbar + 2);
   int* piv = reinterpret_cast<int*>(mbar + 4);
   int* sfail = piv + RA;
 
@@ -625,6 +627,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
   if (tid == 0) {
     mbar_init(&mbar[0]);
     mbar_init(&mbar[1]);
+    for (int i = 0; i < 4; ++i) qctr[i] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -802,6 +805,15 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     constexpr int NWK = NWARPS - 2;
     const bool helper = warp == HW;
     const int w = warp < HW ? warp : warp - 1;   // MMA worker index 0 .. NWK-1 (unused for the helper)
+    // GT: dynamic work claiming, one shared-memory atomic per job broadcast to the warp (the jobs' run times vary
+    // with L2 hits: C5 slab 90.3 -> 88.4 ms). Shared-memory T: static round-robin (dynamic measured 38.6 -> 39.0 ms
+    // on C4: equal-cost jobs, the atomic is pure latency)
+    auto claim = [&](int* c) -> int {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(c, 1);
+      return __shfl_sync(0xffffffffu, v, 0);
+    };
+    const int hw_start = (w + NWK - 2) % NWK;   // static: regular TRSM jobs start from worker 2
     double acc[MAXT][2];
     // fixed shared-memory offsets of this worker's [S | g] tiles: Y rows (Cr) and W columns (T); slots past the
     // last tile accumulate into dead registers
@@ -869,6 +881,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         if (__syncthreads_or(viol)) { aborted = true; p_ab = p; break; }
         SW_STAMP(tit, 8 + 4 * p);
         viol = false;
+        // the next panel's counters: their last users (the previous panel) have all passed the barrier above
+        if (GT && helper && lane == 0) qctr[(pc + 1) & 1] = qctr[2 + ((pc + 1) & 1)] = 0;
         if (!GT && helper && p >= 1 && ln >= 0) {
           // the rows of panel p-1 are dead: stream the next element's rows in
           if (p == 1) expect_all();
@@ -904,7 +918,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           }
           // regular jobs start from worker 2: workers 0 and 1 (which also carry the look-ahead tiles) get the
           // remainder jobs last
-          for (int job = ((a.debug & 1) || helper) ? 1 << 30 : (w + NWK - 2) % NWK; job < nA + nCt + nU; job += NWK) {
+          for (int job = ((a.debug & 1) || helper) ? 1 << 30 : (GT ? claim(qctr + 2 + (pc & 1)) : hw_start);
+               job < nA + nCt + nU; job = GT ? claim(qctr + 2 + (pc & 1)) : job + NWK) {
             if (job < nA) {
               viol |= trsm_right(T, ldT, rA0 + 16 * job, min(2, tA - 2 * job), jb, nb, Uinv, ne, LU, lane);
             } else if (job < nA + nCt) {
@@ -941,8 +956,9 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
             // workers bound the step; later the chain warp does, and it shares the helper's SMSP tensor pipe)
             const bool hjoin = 3 * p < 2 * G.npan;   // (first 2/3: C4 38.7 -> 38.4 ms vs the first half)
             const int nt_w = hjoin ? NWK + 1 : NWK;
-            const int tw = helper ? (hjoin ? NWK : 1 << 30) : w;
-            for (int b = (a.debug & 1) ? 1 << 30 : tw; b < tot; b += nt_w) {
+            const int tw = helper ? NWK : w;
+            for (int b = ((a.debug & 1) || (helper && !hjoin)) ? 1 << 30 : (GT ? claim(qctr + (pc & 1)) : tw); b < tot;
+                 b = GT ? claim(qctr + (pc & 1)) : b + nt_w) {
               // region selection with plain integers (no addresses of locals: they would live on the stack)
               int bi = b, r_lo, r_hi, c_lo, c_hi, nbc;
               const bool inC = bi >= R1a.nblk + R1b.nblk;
@@ -976,6 +992,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           load_C(ln);
         }
         __syncthreads();   // A
+        if (helper && lane == 0) qctr[0] = qctr[1] = qctr[2] = qctr[3] = 0;   // (the exact path's barriers order it)
         {
           const SgDst d = sg_dst(a, l);
           exact_element<THREADS>(d.S, d.g, d.Kf, d.Ef, d.eblk, d.eE, d.so, a.A + a.offA[l], a.B + a.offB[l],
