@@ -24,7 +24,7 @@ constexpr int kLdT = 68;       // row stride of T (>= 64 columns; = 4 mod 16: co
 constexpr int kMaxTiles = 5;   // 8-wide column tiles of [S | g] (n_f + 1 <= 40)
 
 template <int NE, bool FUSED>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseArgs a) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const CondenseArgs a) {
   extern __shared__ __align__(16) double wsm[];
   const int lane = threadIdx.x & 31;
   const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
@@ -44,12 +44,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
     const double* re = a.re + a.offRe[l];
     const double* sh = a.shift ? a.shift + a.offRe[l] : nullptr;   // re-condensation: A_e + diag(shift_e)
     // ---- T = [A | B r], row by row (consecutive lanes read consecutive entries of a row) -----------------------
-    // (eight rows of loads in flight before their shared-memory stores: the generic T pointer could alias the
+    // (a batch of rows' loads in flight before their shared-memory stores: the generic T pointer could alias the
     // global inputs as far as the compiler knows, so load/store pairs would otherwise serialise)
-    for (int i0 = 0; i0 < ne; i0 += 8) {
-      double v0[8], v1[8];
+    constexpr int RB = NE > 16 ? 16 : NE;   // rows per batch (register budget: 4 CTAs of 128 threads per SM)
+    for (int i0 = 0; i0 < ne; i0 += RB) {
+      double v0[RB], v1[RB];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < RB; ++q) {
         const int i = i0 + q;
         const bool rv = i < ne;
         v0[q] = (rv && c0 < ne) ? __ldg(A + i * ne + c0) + ((sh && c0 == i) ? __ldg(sh + i) : 0.0)
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
         v1[q] = (rv && c1 < ne + nf) ? __ldg(Bm + i * nf + c1 - ne) : ((rv && c1 == ne + nf) ? __ldg(re + i) : 0.0);
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < RB; ++q) {
         const int i = i0 + q;
         if (i < ne) {
           T[i * kLdT + c0] = v0[q];
@@ -130,6 +131,28 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
       __syncwarp();
       continue;
     }
+    // ---- [S | g] row-tile operands, one tile ahead: C_e fragments (negated) and the D_e / r_f accumulators; the
+    //      first tile's loads are issued here and land during the triangular solve --------------------------------
+    const double* Cm = a.C + a.offC[l];
+    const double* D = a.D + a.offD[l];
+    const double* rf = a.rf + a.offRf[l];
+    const int RT = (nf + 7) >> 3, CT = (nw + 7) >> 3;
+    auto load_rt = [&](int rt, double (&af)[NE / 4], double (&accs)[kMaxTiles][2]) {
+      const int row = rt * 8 + gid;
+      const bool rv = rt < RT && row < nf;
+#pragma unroll
+      for (int kk = 0; kk < NE / 4; ++kk)
+        af[kk] = (rv && 4 * kk + tig < ne) ? -__ldg(Cm + (int64_t)row * ne + 4 * kk + tig) : 0.0;
+#pragma unroll
+      for (int ct = 0; ct < kMaxTiles; ++ct) {
+        const int c = ct * 8 + 2 * tig;
+        const bool tv = rv && ct < CT;
+        accs[ct][0] = tv ? (c < nf ? __ldg(D + (int64_t)row * nf + c) : (c == nf ? __ldg(rf + row) : 0.0)) : 0.0;
+        accs[ct][1] = tv ? (c + 1 < nf ? __ldg(D + (int64_t)row * nf + c + 1) : (c + 1 == nf ? __ldg(rf + row) : 0.0)) : 0.0;
+      }
+    };
+    double af[NE / 4], accs[kMaxTiles][2];
+    load_rt(0, af, accs);
     // ---- X = U^-1 W: each lane its columns of W ---------------------------------------------------------------------
     {
       const bool a0 = c0 >= ne && c0 < nc, a1 = c1 < nc;
@@ -160,28 +183,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
     }
     __syncwarp();
     // ---- [S | g] = [D | r_f] - C X on DMMA: 8 x 8 tiles, k over n_e (X = columns ne.. of T) --------------------------
-    const double* Cm = a.C + a.offC[l];
     const SgDst dst = FUSED ? sg_dst(a, l) : SgDst{};
-    const double* D = a.D + a.offD[l];
-    const double* rf = a.rf + a.offRf[l];
     const double* X = T + ne;
-    const int RT = (nf + 7) >> 3, CT = (nw + 7) >> 3;
     for (int rt = 0; rt < RT; ++rt) {
       const int row = rt * 8 + gid;
       const bool rv = row < nf;
-      double af[NE / 4];
-#pragma unroll
-      for (int kk = 0; kk < NE / 4; ++kk)
-        af[kk] = (rv && 4 * kk + tig < ne) ? -__ldg(Cm + (int64_t)row * ne + 4 * kk + tig) : 0.0;
-      // all of the row tile's accumulators from D / r_f first (one global latency per row tile, not per tile)
-      double accs[kMaxTiles][2];
-#pragma unroll
-      for (int ct = 0; ct < kMaxTiles; ++ct) {
-        const int c = ct * 8 + 2 * tig;
-        const bool tv = rv && ct < CT;
-        accs[ct][0] = tv ? (c < nf ? __ldg(D + (int64_t)row * nf + c) : (c == nf ? __ldg(rf + row) : 0.0)) : 0.0;
-        accs[ct][1] = tv ? (c + 1 < nf ? __ldg(D + (int64_t)row * nf + c + 1) : (c + 1 == nf ? __ldg(rf + row) : 0.0)) : 0.0;
-      }
+      double afn[NE / 4], accn[kMaxTiles][2];
+      load_rt(rt + 1, afn, accn);   // the next row tile's operands while this one runs (zeros past the last)
 #pragma unroll
       for (int ct = 0; ct < kMaxTiles; ++ct) {
         if (ct >= CT) break;
@@ -213,6 +221,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) warp_kernel(const CondenseA
             }
           }
         }
+      }
+#pragma unroll
+      for (int kk = 0; kk < NE / 4; ++kk) af[kk] = afn[kk];
+#pragma unroll
+      for (int ct = 0; ct < kMaxTiles; ++ct) {
+        accs[ct][0] = accn[ct][0];
+        accs[ct][1] = accn[ct][1];
       }
     }
     __syncwarp();
