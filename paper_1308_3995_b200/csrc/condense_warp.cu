@@ -157,8 +157,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
     {
       const bool a0 = c0 >= ne && c0 < nc, a1 = c1 < nc;
       for (int k = ne - 1; k >= 0; --k) {
-        const double ukk = T[k * kLdT + k];
-        const double x0 = a0 ? T[k * kLdT + c0] / ukk : 0.0, x1 = a1 ? T[k * kLdT + c1] / ukk : 0.0;
+        // one reciprocal per pivot (the back-solve decides nothing: no pivot choice depends on its rounding)
+        const double rk = 1.0 / T[k * kLdT + k];
+        const double x0 = a0 ? T[k * kLdT + c0] * rk : 0.0, x1 = a1 ? T[k * kLdT + c1] * rk : 0.0;
         if (a0) T[k * kLdT + c0] = x0;
         if (a1) T[k * kLdT + c1] = x1;
         for (int i = 0; i < k; ++i) {
