@@ -131,7 +131,8 @@ def main():
     kernels = a.kernel + [None] * (len(a.rep) - len(a.kernel))
     for rep, cfg, kf in zip(a.rep, a.config, kernels):
         m, kname = raw_metrics(rep, kf)
-        short = ("condense_sweep" if "sweep_kernel" in kname else "adjoint" if "adjoint" in kname else
+        short = ("condense_sweep" if "sweep_kernel" in kname else "condense_warp" if "warp_kernel" in kname else
+                 "adjoint" if "adjoint" in kname else
                  "condense" if "condense" in kname else "backsub_saved" if "backsub_saved" in kname else
                  "save_solutions" if "save_kernel" in kname else
                  "backsub" if "backsub" in kname else "".join(ch for ch in kname.split("(")[0][-30:] if ch.isalnum()))
