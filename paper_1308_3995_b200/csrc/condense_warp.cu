@@ -20,7 +20,8 @@ namespace hdg {
 namespace {
 
 constexpr int kWarpsPerCta = 4;
-constexpr int kLdT = 68;       // row stride of T (>= 64 columns; = 4 mod 16: conflict-free DMMA fragment loads)
+constexpr int kLdT = 65;       // row stride of T (>= 64 columns; odd: row-wise (lane = column) and column-wise
+                               // (lane = row) accesses both conflict-free)
 constexpr int kMaxTiles = 5;   // 8-wide column tiles of [S | g] (n_f + 1 <= 40)
 
 template <int NE, bool FUSED>
@@ -69,50 +70,100 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
     int prow = lane;   // original row now at position `lane`
     int fail = 0;
     __syncwarp();
-    // ---- GEPP on T -------------------------------------------------------------------------------------------------
-    for (int k = 0; k < ne; ++k) {
-      // pivot: max |a_ik| over positions i >= k, lowest position on ties (the oracle's strict '>' scan)
-      double best = (lane >= k && lane < ne) ? fabs(T[lane * kLdT + k]) : -1.0;
-      int bi = lane >= k ? lane : 1 << 30;
+    // 8x8-tile DMMA update of T: rows [r0, r0 + 8) (< rlim), columns [cb, cb + 8) (< clim)
+    //   T[rows][cols] -= T[rows][kc .. kc + nk) * T[kr .. kr + nk)[cols]        (nk a multiple of 4, <= 8)
+    auto tile_update = [&](int r0, int rlim, int cb, int clim, int kc, int kr, int nk) {
+      const int row = r0 + gid, col = cb + 2 * tig;
+      const bool rv = row < rlim;
+      double acc[2];
+      acc[0] = (rv && col < clim) ? T[row * kLdT + col] : 0.0;
+      acc[1] = (rv && col + 1 < clim) ? T[row * kLdT + col + 1] : 0.0;
+      const bool bv = cb + gid < clim;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      const int p = bi;
-      if (p != k) {   // warp-uniform
-        double* rk = T + k * kLdT;
-        double* rq = T + p * kLdT;
-        const double t0 = rk[c0], q0 = rq[c0];
-        const double t1 = c1 < kLdT ? rk[c1] : 0.0, q1 = c1 < kLdT ? rq[c1] : 0.0;
-        rk[c0] = q0;
-        rq[c0] = t0;
-        if (c1 < kLdT) {
-          rk[c1] = q1;
-          rq[c1] = t1;
+      for (int kk = 0; kk < 2; ++kk) {
+        if (4 * kk < nk) {
+          const double av = rv ? -T[row * kLdT + kc + 4 * kk + tig] : 0.0;
+          const double bw = bv ? T[(kr + 4 * kk + tig) * kLdT + cb + gid] : 0.0;
+          dmma(acc, av, bw);
         }
-        const int pk = __shfl_sync(0xffffffffu, prow, k), pp = __shfl_sync(0xffffffffu, prow, p);
-        if (lane == k) prow = pp;
-        if (lane == p) prow = pk;
+      }
+      if (rv && col < clim) T[row * kLdT + col] = acc[0];
+      if (rv && col + 1 < clim) T[row * kLdT + col + 1] = acc[1];
+    };
+    // ---- GEPP on T, blocked by 8 columns (right-looking): inside a panel each step is the oracle's — pivot = max
+    //      |a_ik| over positions i >= k with the lowest position on ties, whole rows interchanged, true division for
+    //      the multipliers — with the rank-1 update restricted to the panel's columns (lane = row); then U12 =
+    //      L11^-1 A12 on the panel rows (lane = column) and A22 -= L21 U12 on the FP64 tensor cores. Every pivot
+    //      column is fully updated before its search, so this is GEPP, not a speculation; only the rounding order
+    //      of the trailing sums differs from the oracle's one-step-at-a-time updates ------------------------------
+    for (int k0 = 0; k0 < ne && !fail; k0 += 8) {
+      const int nb = min(8, ne - k0), ke = k0 + nb;
+      for (int k = k0; k < ke; ++k) {
+        // pivot: max |a_ik| over positions i >= k, lowest position on ties (the oracle's strict '>' scan)
+        double best = (lane >= k && lane < ne) ? fabs(T[lane * kLdT + k]) : -1.0;
+        int bi = lane >= k ? lane : 1 << 30;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        const int p = bi;
+        if (p != k) {   // warp-uniform
+          double* rk = T + k * kLdT;
+          double* rq = T + p * kLdT;
+          const double t0 = rk[c0], q0 = rq[c0];
+          const double t1 = c1 < kLdT ? rk[c1] : 0.0, q1 = c1 < kLdT ? rq[c1] : 0.0;
+          rk[c0] = q0;
+          rq[c0] = t0;
+          if (c1 < kLdT) {
+            rk[c1] = q1;
+            rq[c1] = t1;
+          }
+          const int pk = __shfl_sync(0xffffffffu, prow, k), pp = __shfl_sync(0xffffffffu, prow, p);
+          if (lane == k) prow = pp;
+          if (lane == p) prow = pk;
+        }
+        __syncwarp();
+        const double piv = T[k * kLdT + k];
+        if (piv == 0.0 || !(piv == piv)) {   // warp-uniform
+          fail = k + 1;
+          break;
+        }
+        const bool mine = lane > k && lane < ne;
+        double li = 0.0;
+        if (mine) {
+          li = T[lane * kLdT + k] / piv;   // multipliers (true division, as the oracle)
+          T[lane * kLdT + k] = li;
+        }
+        for (int j = k + 1; j < ke; ++j) {   // the panel's columns only (lane = row)
+          const double u = T[k * kLdT + j];
+          if (mine) T[lane * kLdT + j] = fma(-li, u, T[lane * kLdT + j]);
+        }
+        __syncwarp();
+      }
+      if (fail) break;
+      // U12 = L11^-1 A12: the panel rows over columns [ke, nc) (lane = column, unit lower L11 by broadcast)
+      for (int c = ke + lane; c < nc; c += 32) {
+        double t[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) t[r] = r < nb ? T[(k0 + r) * kLdT + c] : 0.0;
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {
+          if (r < nb) {
+#pragma unroll
+            for (int q = 0; q < r; ++q) t[r] = fma(-T[(k0 + r) * kLdT + k0 + q], t[q], t[r]);
+            T[(k0 + r) * kLdT + c] = t[r];
+          }
+        }
       }
       __syncwarp();
-      const double piv = T[k * kLdT + k];
-      if (piv == 0.0 || !(piv == piv)) {   // warp-uniform
-        fail = k + 1;
-        break;
+      // A22 -= L21 U12 over rows [ke, ne), columns [ke, nc): 8x8 DMMA tiles, k = the panel width
+      if (ke < ne) {
+        const int ntc = (nc - ke + 7) >> 3, ntile = ((ne - ke + 7) >> 3) * ntc;
+        for (int q = 0; q < ntile; ++q) tile_update(ke + (q / ntc) * 8, ne, ke + (q % ntc) * 8, nc, k0, k0, nb);
+        __syncwarp();
       }
-      if (lane > k && lane < ne) T[lane * kLdT + k] /= piv;   // multipliers (true division, as the oracle)
-      __syncwarp();
-      // rank-1 update of rows k+1.. over this lane's columns > k
-      const bool a0 = c0 > k && c0 < nc, a1 = c1 < nc;
-      const double u0 = a0 ? T[k * kLdT + c0] : 0.0, u1 = a1 ? T[k * kLdT + c1] : 0.0;
-      for (int i = k + 1; i < ne; ++i) {
-        const double li = T[i * kLdT + k];
-        if (a0) T[i * kLdT + c0] = fma(-li, u0, T[i * kLdT + c0]);
-        if (a1) T[i * kLdT + c1] = fma(-li, u1, T[i * kLdT + c1]);
-      }
-      __syncwarp();
     }
     // ---- factors: L\U rows in GEPP order (row-major, coalesced per row) + the permutation — also for a singular
     //      element (its partial factors; prow is a permutation however far the elimination got), so the factor
@@ -153,19 +204,35 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
     };
     double af[NE / 4], accs[kMaxTiles][2];
     load_rt(0, af, accs);
-    // ---- X = U^-1 W: each lane its columns of W ---------------------------------------------------------------------
+    // ---- X = U^-1 W, blocked by 8 rows from the bottom: the diagonal 8x8 triangle per W column (lane = column, one
+    //      reciprocal per pivot: the back-solve decides nothing), then the rows above -= U12 X_b on DMMA tiles ------
     {
       const bool a0 = c0 >= ne && c0 < nc, a1 = c1 < nc;
-      for (int k = ne - 1; k >= 0; --k) {
-        // one reciprocal per pivot (the back-solve decides nothing: no pivot choice depends on its rounding)
-        const double rk = 1.0 / T[k * kLdT + k];
-        const double x0 = a0 ? T[k * kLdT + c0] * rk : 0.0, x1 = a1 ? T[k * kLdT + c1] * rk : 0.0;
-        if (a0) T[k * kLdT + c0] = x0;
-        if (a1) T[k * kLdT + c1] = x1;
-        for (int i = 0; i < k; ++i) {
-          const double u = T[i * kLdT + k];
-          if (a0) T[i * kLdT + c0] = fma(-u, x0, T[i * kLdT + c0]);
-          if (a1) T[i * kLdT + c1] = fma(-u, x1, T[i * kLdT + c1]);
+      for (int r0 = (ne - 1) & ~7; r0 >= 0; r0 -= 8) {
+        const int nr = min(8, ne - r0);
+        double rd[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) rd[r] = r < nr ? 1.0 / T[(r0 + r) * kLdT + r0 + r] : 0.0;
+        for (int c = ne + lane; c < nc; c += 32) {
+          double t[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) t[r] = r < nr ? T[(r0 + r) * kLdT + c] : 0.0;
+#pragma unroll
+          for (int r = 7; r >= 0; --r) {
+            if (r < nr) {
+#pragma unroll
+              for (int q = r + 1; q < 8; ++q)
+                if (q < nr) t[r] = fma(-T[(r0 + r) * kLdT + r0 + q], t[q], t[r]);
+              t[r] *= rd[r];
+              T[(r0 + r) * kLdT + c] = t[r];
+            }
+          }
+        }
+        __syncwarp();
+        if (r0 > 0) {
+          const int ntc = (nw + 7) >> 3, ntile = (r0 >> 3) * ntc;
+          for (int q = 0; q < ntile; ++q) tile_update((q / ntc) * 8, r0, ne + (q % ntc) * 8, nc, r0, r0, nr);
+          __syncwarp();
         }
       }
       if (a.Xout) {   // §8(f) NEXT #2: the local solutions X = A^-1 [B | r_e] (columns ne .. nc of T) — save them
