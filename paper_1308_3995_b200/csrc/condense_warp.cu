@@ -34,13 +34,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
   double* T = wsm + (size_t)w * NE * kLdT;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerCta;
   const int c0 = lane, c1 = lane + 32;   // this lane's columns of T
+  // element l's A_e into T's columns [0, ne) by asynchronous 8-byte copies (no registers, no wait here)
+  auto copy_A = [&](int64_t l_) {
+    if (lane < ne) {
+      const double* A_ = a.A + a.offA[l_];
+      for (int i = 0; i < ne; ++i)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(T + i * kLdT + lane)),
+                     "l"(A_ + (int64_t)i * ne + lane) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  bool pref = false;   // this element's A_e already in flight (issued during the previous element's [S | g] tiles)
   for (int64_t it = (int64_t)blockIdx.x * kWarpsPerCta + w; it < a.count; it += nwarps) {
     const int64_t l = a.elems ? a.elems[it] : it;
     // no L2 prefetch: measured on C2, the next element's blocks prefetched at this element's start 0.673 ms (ncu:
     // 22 % L2 hit rate, 1.76x the algorithmic DRAM reads — an element's run time ahead, the lines were evicted
     // before use), a short-distance schedule (this element's C_e, D_e at its start, the next A_e, B_e before the
-    // [S | g] tiles) 0.639 ms, none 0.629 ms (C1 0.0399 / 0.0418 / 0.0397 ms)
-    const double* A = a.A + a.offA[l];
+    // [S | g] tiles) 0.639 ms, none 0.629 ms (C1 0.0399 / 0.0418 / 0.0397 ms). Instead the next element's A_e is
+    // copied straight into T's dead A columns while this element's [S | g] tiles run.
+    if (!pref) copy_A(l);
+    pref = false;
     const double* Bm = a.B + a.offB[l];
     const double* re = a.re + a.offRe[l];
     const double* sh = a.shift ? a.shift + a.offRe[l] : nullptr;   // re-condensation: A_e + diag(shift_e)
@@ -54,19 +67,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
       for (int q = 0; q < RB; ++q) {
         const int i = i0 + q;
         const bool rv = i < ne;
-        v0[q] = (rv && c0 < ne) ? __ldg(A + i * ne + c0) + ((sh && c0 == i) ? __ldg(sh + i) : 0.0)
-                                : ((rv && c0 < ne + nf) ? __ldg(Bm + i * nf + c0 - ne) : ((rv && c0 == ne + nf) ? __ldg(re + i) : 0.0));
+        v0[q] = (rv && c0 >= ne && c0 < ne + nf) ? __ldg(Bm + i * nf + c0 - ne) : ((rv && c0 == ne + nf) ? __ldg(re + i) : 0.0);
         v1[q] = (rv && c1 < ne + nf) ? __ldg(Bm + i * nf + c1 - ne) : ((rv && c1 == ne + nf) ? __ldg(re + i) : 0.0);
       }
 #pragma unroll
       for (int q = 0; q < RB; ++q) {
         const int i = i0 + q;
         if (i < ne) {
-          T[i * kLdT + c0] = v0[q];
+          if (c0 >= ne) T[i * kLdT + c0] = v0[q];
           if (c1 < kLdT) T[i * kLdT + c1] = v1[q];
         }
       }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // A_e has landed (this lane's copies)
+    if (sh && lane < ne) T[lane * kLdT + lane] += __ldg(sh + lane);   // re-condensation: A_e + diag(shift_e)
     int prow = lane;   // original row now at position `lane`
     int fail = 0;
     __syncwarp();
@@ -234,6 +248,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
           for (int q = 0; q < ntile; ++q) tile_update((q / ntc) * 8, r0, ne + (q % ntc) * 8, nc, r0, r0, nr);
           __syncwarp();
         }
+      }
+      __syncwarp();   // every read of T's A columns (U) is done
+      if (it + nwarps < a.count) {
+        copy_A(a.elems ? a.elems[it + nwarps] : it + nwarps);
+        pref = true;
       }
       if (a.Xout) {   // §8(f) NEXT #2: the local solutions X = A^-1 [B | r_e] (columns ne .. nc of T) — save them
         __syncwarp();
