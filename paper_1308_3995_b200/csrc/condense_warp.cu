@@ -57,29 +57,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
     const double* Bm = a.B + a.offB[l];
     const double* re = a.re + a.offRe[l];
     const double* sh = a.shift ? a.shift + a.offRe[l] : nullptr;   // re-condensation: A_e + diag(shift_e)
-    // ---- T = [A | B r], row by row (consecutive lanes read consecutive entries of a row) -----------------------
-    // (a batch of rows' loads in flight before their shared-memory stores: the generic T pointer could alias the
-    // global inputs as far as the compiler knows, so load/store pairs would otherwise serialise)
-    constexpr int RB = NE > 16 ? 16 : NE;   // rows per batch (register budget: 4 CTAs of 128 threads per SM)
-    for (int i0 = 0; i0 < ne; i0 += RB) {
-      double v0[RB], v1[RB];
+    // ---- W = [B_e | r_e] into T's columns [ne, nc) by asynchronous 8-byte copies: they land while the
+    //      elimination of A_e runs (the row interchanges and L^-1 reach W only after it) ---------------------------
+    {
 #pragma unroll
-      for (int q = 0; q < RB; ++q) {
-        const int i = i0 + q;
-        const bool rv = i < ne;
-        v0[q] = (rv && c0 >= ne && c0 < ne + nf) ? __ldg(Bm + i * nf + c0 - ne) : ((rv && c0 == ne + nf) ? __ldg(re + i) : 0.0);
-        v1[q] = (rv && c1 < ne + nf) ? __ldg(Bm + i * nf + c1 - ne) : ((rv && c1 == ne + nf) ? __ldg(re + i) : 0.0);
-      }
-#pragma unroll
-      for (int q = 0; q < RB; ++q) {
-        const int i = i0 + q;
-        if (i < ne) {
-          if (c0 >= ne) T[i * kLdT + c0] = v0[q];
-          if (c1 < kLdT) T[i * kLdT + c1] = v1[q];
+      for (int h = 0; h < 2; ++h) {
+        const int c = h ? c1 : c0;
+        if (c >= ne && c < nc) {
+          const bool isr = c == ne + nf;
+          for (int i = 0; i < ne; ++i)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(T + i * kLdT + c)),
+                         "l"(isr ? re + i : Bm + (int64_t)i * nf + (c - ne)) : "memory");
         }
       }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // A_e has landed (this lane's copies)
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // A_e has landed (this lane's copies; W may not)
     if (sh && lane < ne) T[lane * kLdT + lane] += __ldg(sh + lane);   // re-condensation: A_e + diag(shift_e)
     int prow = lane;   // original row now at position `lane`
     int fail = 0;
@@ -104,6 +97,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
       if (rv && col < clim) T[row * kLdT + col] = acc[0];
       if (rv && col + 1 < clim) T[row * kLdT + col + 1] = acc[1];
     };
+    // one panel of a unit-lower block solve: rows [k0, k0 + nb) <- L11^-1 rows (lane = column, L11 by broadcast), then
+    // rows [k0 + nb, ne) -= L21 * those rows on 8x8 DMMA tiles (k = nb); columns [cb, ce)
+    auto lower_panel = [&](int k0, int nb, int cb, int ce) {
+      for (int c = cb + lane; c < ce; c += 32) {
+        double t[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) t[r] = r < nb ? T[(k0 + r) * kLdT + c] : 0.0;
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {
+          if (r < nb) {
+#pragma unroll
+            for (int q = 0; q < r; ++q) t[r] = fma(-T[(k0 + r) * kLdT + k0 + q], t[q], t[r]);
+            T[(k0 + r) * kLdT + c] = t[r];
+          }
+        }
+      }
+      __syncwarp();
+      const int ke = k0 + nb;
+      if (ke < ne && cb < ce) {
+        const int ntc = (ce - cb + 7) >> 3, ntile = ((ne - ke + 7) >> 3) * ntc;
+        for (int q = 0; q < ntile; ++q) tile_update(ke + (q / ntc) * 8, ne, cb + (q % ntc) * 8, ce, k0, k0, nb);
+        __syncwarp();
+      }
+    };
     // ---- GEPP on T, blocked by 8 columns (right-looking): inside a panel each step is the oracle's — pivot = max
     //      |a_ik| over positions i >= k with the lowest position on ties, whole rows interchanged, true division for
     //      the multipliers — with the rank-1 update restricted to the panel's columns (lane = row); then U12 =
@@ -124,15 +141,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
         }
         const int p = bi;
         if (p != k) {   // warp-uniform
-          double* rk = T + k * kLdT;
-          double* rq = T + p * kLdT;
-          const double t0 = rk[c0], q0 = rq[c0];
-          const double t1 = c1 < kLdT ? rk[c1] : 0.0, q1 = c1 < kLdT ? rq[c1] : 0.0;
-          rk[c0] = q0;
-          rq[c0] = t0;
-          if (c1 < kLdT) {
-            rk[c1] = q1;
-            rq[c1] = t1;
+          if (c0 < ne) {   // A's columns only: W takes the final permutation after the elimination
+            double* rk = T + k * kLdT;
+            double* rq = T + p * kLdT;
+            const double t0 = rk[c0], q0 = rq[c0];
+            rk[c0] = q0;
+            rq[c0] = t0;
           }
           const int pk = __shfl_sync(0xffffffffu, prow, k), pp = __shfl_sync(0xffffffffu, prow, p);
           if (lane == k) prow = pp;
@@ -157,27 +171,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
         __syncwarp();
       }
       if (fail) break;
-      // U12 = L11^-1 A12: the panel rows over columns [ke, nc) (lane = column, unit lower L11 by broadcast)
-      for (int c = ke + lane; c < nc; c += 32) {
-        double t[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) t[r] = r < nb ? T[(k0 + r) * kLdT + c] : 0.0;
-#pragma unroll
-        for (int r = 1; r < 8; ++r) {
-          if (r < nb) {
-#pragma unroll
-            for (int q = 0; q < r; ++q) t[r] = fma(-T[(k0 + r) * kLdT + k0 + q], t[q], t[r]);
-            T[(k0 + r) * kLdT + c] = t[r];
-          }
-        }
-      }
-      __syncwarp();
-      // A22 -= L21 U12 over rows [ke, ne), columns [ke, nc): 8x8 DMMA tiles, k = the panel width
-      if (ke < ne) {
-        const int ntc = (nc - ke + 7) >> 3, ntile = ((ne - ke + 7) >> 3) * ntc;
-        for (int q = 0; q < ntile; ++q) tile_update(ke + (q / ntc) * 8, ne, ke + (q % ntc) * 8, nc, k0, k0, nb);
-        __syncwarp();
-      }
+      lower_panel(k0, nb, ke, ne);   // U12 = L11^-1 A12, A22 -= L21 U12 over A's columns
     }
     // ---- factors: L\U rows in GEPP order (row-major, coalesced per row) + the permutation — also for a singular
     //      element (its partial factors; prow is a permutation however far the elimination got), so the factor
@@ -193,9 +187,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
       const SgDst dst = sg_dst(a, l);
       for (int i = lane; i < nf * nf; i += 32) out_S1(dst, nf, i / nf, i % nf, nan);
       for (int i = lane; i < nf; i += 32) out_g(dst, i, nan);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");   // W's copies must land before T is reused
       __syncwarp();
       continue;
     }
+    // ---- W <- L^-1 P W: W's copies have landed; rows into GEPP order (position i <- original row prow[i]), then
+    //      the unit-lower solve panel by panel -----------------------------------------------------------------------
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = h ? c1 : c0;
+      const bool act = c >= ne && c < nc;
+      double v[NE];
+#pragma unroll
+      for (int i = 0; i < NE; ++i) {
+        const int src = __shfl_sync(0xffffffffu, prow, i);
+        v[i] = (act && i < ne) ? T[src * kLdT + c] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NE; ++i)
+        if (act && i < ne) T[i * kLdT + c] = v[i];
+    }
+    __syncwarp();
+    for (int k0 = 0; k0 < ne; k0 += 8) lower_panel(k0, min(8, ne - k0), ne, nc);
     // ---- [S | g] row-tile operands, one tile ahead: C_e fragments (negated) and the D_e / r_f accumulators; the
     //      first tile's loads are issued here and land during the triangular solve --------------------------------
     const double* Cm = a.C + a.offC[l];
