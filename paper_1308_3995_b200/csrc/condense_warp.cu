@@ -100,16 +100,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
     // one panel of a unit-lower block solve: rows [k0, k0 + nb) <- L11^-1 rows (lane = column, L11 by broadcast), then
     // rows [k0 + nb, ne) -= L21 * those rows on 8x8 DMMA tiles (k = nb); columns [cb, ce)
     auto lower_panel = [&](int k0, int nb, int cb, int ce) {
-      for (int c = cb + lane; c < ce; c += 32) {
-        double t[8];
+      {   // columns cb + lane and cb + lane + 32 together: one broadcast load of L11 feeds both
+        const int ca = cb + lane, cc = cb + lane + 32;
+        const bool h0 = ca < ce, h1 = cc < ce;
+        double t[8], v[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) t[r] = r < nb ? T[(k0 + r) * kLdT + c] : 0.0;
+        for (int r = 0; r < 8; ++r) {
+          t[r] = (h0 && r < nb) ? T[(k0 + r) * kLdT + ca] : 0.0;
+          v[r] = (h1 && r < nb) ? T[(k0 + r) * kLdT + cc] : 0.0;
+        }
 #pragma unroll
         for (int r = 1; r < 8; ++r) {
           if (r < nb) {
 #pragma unroll
-            for (int q = 0; q < r; ++q) t[r] = fma(-T[(k0 + r) * kLdT + k0 + q], t[q], t[r]);
-            T[(k0 + r) * kLdT + c] = t[r];
+            for (int q = 0; q < r; ++q) {
+              const double lq = T[(k0 + r) * kLdT + k0 + q];
+              t[r] = fma(-lq, t[q], t[r]);
+              v[r] = fma(-lq, v[q], v[r]);
+            }
+            if (h0) T[(k0 + r) * kLdT + ca] = t[r];
+            if (h1) T[(k0 + r) * kLdT + cc] = v[r];
           }
         }
       }
@@ -130,16 +140,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
     for (int k0 = 0; k0 < ne && !fail; k0 += 8) {
       const int nb = min(8, ne - k0), ke = k0 + nb;
       for (int k = k0; k < ke; ++k) {
-        // pivot: max |a_ik| over positions i >= k, lowest position on ties (the oracle's strict '>' scan)
-        double best = (lane >= k && lane < ne) ? fabs(T[lane * kLdT + k]) : -1.0;
-        int bi = lane >= k ? lane : 1 << 30;
+        // pivot: max |a_ik| over positions i >= k, lowest position on ties (the oracle's strict '>' scan): the
+        // maximum by a butterfly, then the lowest candidate lane holding it by a ballot (NaNs never win; all-NaN
+        // candidates leave the pivot in place and fail below)
+        const double mag = (lane >= k && lane < ne) ? fabs(T[lane * kLdT + k]) : -1.0;
+        double best = mag;
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-        }
-        const int p = bi;
+        for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
+        const unsigned hit = __ballot_sync(0xffffffffu, lane >= k && lane < ne && mag == best);
+        const int p = hit ? __ffs(hit) - 1 : k;
         if (p != k) {   // warp-uniform
           if (c0 < ne) {   // A's columns only: W takes the final permutation after the elimination
             double* rk = T + k * kLdT;
@@ -239,21 +248,33 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 4) warp_kernel(const Conden
       const bool a0 = c0 >= ne && c0 < nc, a1 = c1 < nc;
       for (int r0 = (ne - 1) & ~7; r0 >= 0; r0 -= 8) {
         const int nr = min(8, ne - r0);
+        const double rdl = lane < nr ? 1.0 / T[(r0 + lane) * kLdT + r0 + lane] : 0.0;   // one reciprocal per lane
         double rd[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) rd[r] = r < nr ? 1.0 / T[(r0 + r) * kLdT + r0 + r] : 0.0;
-        for (int c = ne + lane; c < nc; c += 32) {
-          double t[8];
+        for (int r = 0; r < 8; ++r) rd[r] = __shfl_sync(0xffffffffu, rdl, r);
+        {   // this lane's W columns c0 (if >= ne) and c1 together: one broadcast load of U feeds both
+          const bool h0 = c0 >= ne && c0 < nc, h1 = c1 < nc;
+          double t[8], v[8];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) t[r] = r < nr ? T[(r0 + r) * kLdT + c] : 0.0;
+          for (int r = 0; r < 8; ++r) {
+            t[r] = (h0 && r < nr) ? T[(r0 + r) * kLdT + c0] : 0.0;
+            v[r] = (h1 && r < nr) ? T[(r0 + r) * kLdT + c1] : 0.0;
+          }
 #pragma unroll
           for (int r = 7; r >= 0; --r) {
             if (r < nr) {
 #pragma unroll
-              for (int q = r + 1; q < 8; ++q)
-                if (q < nr) t[r] = fma(-T[(r0 + r) * kLdT + r0 + q], t[q], t[r]);
+              for (int q = r + 1; q < 8; ++q) {
+                if (q < nr) {
+                  const double u = T[(r0 + r) * kLdT + r0 + q];
+                  t[r] = fma(-u, t[q], t[r]);
+                  v[r] = fma(-u, v[q], v[r]);
+                }
+              }
               t[r] *= rd[r];
-              T[(r0 + r) * kLdT + c] = t[r];
+              v[r] *= rd[r];
+              if (h0) T[(r0 + r) * kLdT + c0] = t[r];
+              if (h1) T[(r0 + r) * kLdT + c1] = v[r];
             }
           }
         }
