@@ -63,7 +63,14 @@ __global__ void __launch_bounds__(128) bjacobi_setup_kernel(const double* K, dou
   double* M = M_s[w];
   constexpr int ld = 49;   // [K_ff | I]: 2 n <= 48 columns
   int q = row_ptr[r];
-  while (col_idx[q] != (int32_t)f) ++q;   // the diagonal block (always present)
+  const int qe = row_ptr[r + 1];
+  while (q < qe && col_idx[q] != (int32_t)f) ++q;   // the diagonal block (present in every owned row)
+  if (q == qe) {   // (defensive: no diagonal block — the preconditioner skips the row)
+    double* D = Dinv + dinv_off[r];
+    for (int i = 0; i < n; ++i)
+      for (int j = lane; j < n; j += 32) D[i * n + j] = i == j ? 1.0 : 0.0;
+    return;
+  }
   const double* Kb = K + blk_off[q];
   for (int i = 0; i < n; ++i) {
     for (int j = lane; j < 2 * n; j += 32) M[i * ld + j] = j < n ? Kb[i * n + j] : (j - n == i ? 1.0 : 0.0);
@@ -207,6 +214,7 @@ cudaError_t skeleton_gmres(const Plan& p, SolverWork& sw, const double* K, const
   if (sw.n != n || sw.m != m) {
     cudaFree(sw.V); cudaFree(sw.w); cudaFree(sw.z); cudaFree(sw.partial); cudaFree(sw.h); cudaFree(sw.Dinv);
     cudaFree(sw.dinv_off);
+    cudaFree(sw.xfull); cudaFree(sw.hsend); cudaFree(sw.hrecv); cudaFree(sw.d_hsend_idx); cudaFree(sw.d_hrecv_idx);
     sw = SolverWork();
     std::vector<int64_t> doff(nrows + 1, 0);
     std::vector<int32_t> fnd(p.F);
