@@ -3,6 +3,8 @@ import ctypes
 import os
 import re
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -54,3 +56,14 @@ def test_product_has_no_oracle_dependency():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f
                 assert "import gen" not in txt and "philox_normal.h" not in txt, f
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No CPU fallback: with libhdg.so absent the binding raises instead of computing anything."""
+    import paper_1308_3995_b200 as hdg
+    monkeypatch.setattr(hdg, "_lib", None)
+    monkeypatch.setattr(hdg, "LIB_PATH", "/nonexistent/libhdg.so")
+    with pytest.raises(ImportError):
+        hdg.lib()
+    with pytest.raises(ImportError):
+        hdg.Context(0)
