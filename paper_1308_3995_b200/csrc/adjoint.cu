@@ -99,9 +99,15 @@ __device__ __forceinline__ void solve_transposed(const double* LU, const int32_t
     for (int j = 0; j < 8; ++j)
       Uc[j] = (lane < 8 && r < ne && j <= i && r0 + j < ne) ? __ldg(LU + (int64_t)(r0 + j) * ne + r) : 0.0;
     double vi = (lane < 8 && r < ne) ? vec[r] - s : 0.0;
+    // the row's reciprocal pivot, off the dependency chain (as in the primal back-substitution)
+    double di = 1.0;   // Uc[i] (static selects: a dynamic index would put Uc in local memory)
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j == i && lane < 8 && r < ne) di = Uc[j];
+    const double rdi = 1.0 / di;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      if (i == j && lane < 8 && r < ne) vi = vi / Uc[j];
+      if (i == j && lane < 8 && r < ne) vi *= rdi;
       const double vj = __shfl_sync(0xffffffffu, vi, j);
       if (j < i) vi = fma(-Uc[j], vj, vi);
     }
@@ -143,7 +149,7 @@ __device__ __forceinline__ void solve_transposed(const double* LU, const int32_t
 
 // MODE 0: g~_e = r~_f - B_e^T A_e^-T r~_e.  MODE 1: u~_e = A_e^-T (r~_e - C_e^T lambda~_e).
 template <int MODE>
-__global__ void __launch_bounds__(kWarps * 32) adjoint_kernel(const AdjointArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 4) adjoint_kernel(const AdjointArgs a) {
   __shared__ double vec_s[kWarps][kMaxNe + 8];
   __shared__ double z_s[kWarps][kMaxNe + 8];
   __shared__ double lam_s[kWarps][kMaxNf + 8];

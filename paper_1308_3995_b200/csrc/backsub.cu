@@ -132,9 +132,12 @@ __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs 
 #pragma unroll
       for (int j = 0; j < 8; ++j) Ur[j] = (lane < 8 && r < ne && j >= i && r0 + j < ne) ? __ldg(LU + (int64_t)r * ne + r0 + j) : 0.0;
       double xi = (lane < 8 && r < ne) ? y[r] - s : 0.0;
+      // the row's reciprocal pivot, off the dependency chain (a division inside it stalled every step and split
+      // lanes 0-7 on its slow path)
+      const double rdi = (lane < 8 && r < ne) ? 1.0 / __ldg(LU + (int64_t)r * ne + r) : 1.0;
 #pragma unroll
       for (int j = 7; j >= 0; --j) {
-        if (i == j && lane < 8 && r < ne) xi = xi / Ur[j];
+        if (i == j && lane < 8 && r < ne) xi *= rdi;
         const double xj = __shfl_sync(0xffffffffu, xi, j);
         if (j > i && r0 + j < ne) xi = fma(-Ur[j], xj, xi);
       }
