@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) adjoint_kernel(const AdjointAr
         if (q < nf) {
           int s2 = 0, qq = q;
           if (qq >= n[0]) { qq -= n[0]; s2 = 1; if (qq >= n[1]) { qq -= n[1]; s2 = 2; } }
-          v = __ldg(a.lambda + a.face_off[f[s2]] + qq);
+          v = __ldg(a.lambda + a.face_off[s2 == 0 ? f[0] : (s2 == 1 ? f[1] : f[2])] + qq);
         }
         lam[q] = v;
       }

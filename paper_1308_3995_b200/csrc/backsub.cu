@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kWarps * 32) backsub_kernel(const BacksubArgs 
         if (q < nf) {
           int s = 0, qq = q;
           if (qq >= n[0]) { qq -= n[0]; s = 1; if (qq >= n[1]) { qq -= n[1]; s = 2; } }
-          v = __ldg(a.lambda + a.face_off[f[s]] + qq);
+          v = __ldg(a.lambda + a.face_off[s == 0 ? f[0] : (s == 1 ? f[1] : f[2])] + qq);
         }
         lam[q] = v;
       }
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) backsub_rows_kernel(const
       for (int q = lane; q < nf; q += 32) {
         int s = 0, qq = q;
         if (qq >= n[0]) { qq -= n[0]; s = 1; if (qq >= n[1]) { qq -= n[1]; s = 2; } }
-        lam_s[w][q] = __ldg(a.lambda + a.face_off[f[s]] + qq);
+        lam_s[w][q] = __ldg(a.lambda + a.face_off[s == 0 ? f[0] : (s == 1 ? f[1] : f[2])] + qq);
       }
     }
     __syncwarp();

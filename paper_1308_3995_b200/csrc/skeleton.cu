@@ -119,9 +119,10 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs a) {
   if (q >= a.nnzb) return;
   const int32_t f = a.blk_row[q], c = a.col_idx[q];
   const int na = a.face_ndof[f], nb = a.face_ndof[c];
-  const double* src[2] = {nullptr, nullptr};
-  int ld[2] = {0, 0};
-  int ns = 0;
+  // the (at most two) contributing elements, left first; scalars, not arrays indexed by the running count (those
+  // went to local memory)
+  const double *src0 = nullptr, *src1 = nullptr;
+  int ld0 = 0, ld1 = 0, ns = 0;
 #pragma unroll
   for (int side = 0; side < 2; ++side) {
     const int32_t e = a.face_elem[2 * (int64_t)f + side];
@@ -130,8 +131,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs a) {
     if (slot_of(a.elem_face, a.face_ndof, e, f, &so_a) < 0) continue;
     if (slot_of(a.elem_face, a.face_ndof, e, c, &so_b) < 0) continue;
     const int64_t l = e - a.eb;
-    ld[ns] = a.nf[l];
-    src[ns] = TR ? a.S + a.offS[l] + (int64_t)so_b * ld[ns] + so_a : a.S + a.offS[l] + (int64_t)so_a * ld[ns] + so_b;
+    const int ldl = a.nf[l];
+    const double* sp = TR ? a.S + a.offS[l] + (int64_t)so_b * ldl + so_a : a.S + a.offS[l] + (int64_t)so_a * ldl + so_b;
+    if (ns == 0) { src0 = sp; ld0 = ldl; } else { src1 = sp; ld1 = ldl; }
     ++ns;
   }
   double* dst = a.K + a.blk_off[q];
@@ -139,8 +141,8 @@ __global__ void __launch_bounds__(256) assemble_kernel(const AsmArgs a) {
   const int step_r = 32 / nb, step_c = 32 - (32 / nb) * nb;
   for (int idx = lane; idx < na * nb; idx += 32) {
     double v = 0.0;
-    if (ns > 0) v = v + __ldg(TR ? src[0] + (int64_t)cc * ld[0] + r : src[0] + (int64_t)r * ld[0] + cc);
-    if (ns > 1) v = v + __ldg(TR ? src[1] + (int64_t)cc * ld[1] + r : src[1] + (int64_t)r * ld[1] + cc);
+    if (ns > 0) v = v + __ldg(TR ? src0 + (int64_t)cc * ld0 + r : src0 + (int64_t)r * ld0 + cc);
+    if (ns > 1) v = v + __ldg(TR ? src1 + (int64_t)cc * ld1 + r : src1 + (int64_t)r * ld1 + cc);
     dst[idx] = v;
     r += step_r;
     cc += step_c;
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(const AsmArgs a) {
   const int64_t f = a.f0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (f >= a.f1) return;
   const int na = a.face_ndof[f];
-  const double* src[2] = {nullptr, nullptr};
+  const double *src0 = nullptr, *src1 = nullptr;
   int ns = 0;
 #pragma unroll
   for (int side = 0; side < 2; ++side) {
@@ -165,13 +167,15 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(const AsmArgs a) {
     if (e < a.eb || e >= a.eb + a.n) continue;
     int so = 0;
     if (slot_of(a.elem_face, a.face_ndof, e, (int32_t)f, &so) < 0) continue;
-    src[ns++] = a.g + a.offG[e - a.eb] + so;
+    const double* sp = a.g + a.offG[e - a.eb] + so;
+    if (ns == 0) src0 = sp; else src1 = sp;
+    ++ns;
   }
   double* dst = a.E + (a.face_off[f] - a.tr0);
   for (int i = lane; i < na; i += 32) {
     double v = 0.0;
-    if (ns > 0) v = v + __ldg(src[0] + i);
-    if (ns > 1) v = v + __ldg(src[1] + i);
+    if (ns > 0) v = v + __ldg(src0 + i);
+    if (ns > 1) v = v + __ldg(src1 + i);
     dst[i] = v;
   }
 }
