@@ -828,6 +828,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       offW[s] = CB + (t % G.CTs) * 8 + gid + tig * ldT;
       offD[s] = (t0 < G.ntiles && row < nf) ? (c < nf ? row * nf + c : (c == nf ? -(row + 2) : -1)) : -1;
     }
+    double rv[(kMaxNe + 31) / 32];   // helper: the next element's r_e column, loaded ahead
+    bool have_rv = false;
     for (int64_t it = blockIdx.x; it < a.count; it += gridDim.x, ph ^= 1u) {
       const int64_t l = elem_of(it);
       const int64_t next = it + gridDim.x;
@@ -846,10 +848,14 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         // the r_e column: every load issued before the first shared store (the generic T pointer could alias the
         // global input as far as the compiler knows: interleaved load/store pairs serialise on the HBM latency —
         // measured, the helper reached the first panel barrier 3-6 K cycles after the workers)
-        const double* re = a.re + a.offRe[l];
-        double rv[(kMaxNe + 31) / 32];
+        // (loaded before the previous element's last barrier when there was one: its HBM latency then overlaps the
+        // end of that element instead of holding the first panel barrier)
+        if (!have_rv) {
+          const double* re = a.re + a.offRe[l];
 #pragma unroll
-        for (int q = 0; q < (kMaxNe + 31) / 32; ++q) rv[q] = lane + 32 * q < ne ? __ldg(re + lane + 32 * q) : 0.0;
+          for (int q = 0; q < (kMaxNe + 31) / 32; ++q) rv[q] = lane + 32 * q < ne ? __ldg(re + lane + 32 * q) : 0.0;
+        }
+        have_rv = false;
 #pragma unroll
         for (int q = 0; q < (kMaxNe + 31) / 32; ++q)
           if (lane + 32 * q < ne) T[(size_t)(lane + 32 * q) * ldT + CB + nf] = rv[q];
@@ -1006,6 +1012,12 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           int32_t* perm = reinterpret_cast<int32_t*>(LU + (size_t)ne * ne);
           for (int i = lane; i < ne; i += 32) perm[i] = i;
           if (lane == 0) a.info[l] = 0;
+          if (!GT && ln >= 0) {   // the next element's r_e column, landing while the workers store [S | g]
+            const double* re = a.re + a.offRe[ln];
+#pragma unroll
+            for (int q = 0; q < (kMaxNe + 31) / 32; ++q) rv[q] = lane + 32 * q < ne ? __ldg(re + lane + 32 * q) : 0.0;
+            have_rv = true;
+          }
         } else {
           if constexpr (FUSED) {   // hdg_condense_assemble: straight into K, E
             const SgDst dst = sg_dst(a, l);
