@@ -819,9 +819,13 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     // last tile accumulate into dead registers
     // offD[s]: D_e offset of this lane's accumulator pair (>= 0), -(row + 2) for the r_f column, -1 for padding
     int offY[MAXT], offW[MAXT], offD[MAXT];
+    // row map: when the [S | g] tile rows are exactly the MMA workers and a row's column tiles fill the slots (C4:
+    // 6 x 7 tiles), worker w owns tile row w, so one Y_p fragment per k-step serves all its slots (8 shared loads
+    // per 7 DMMAs instead of 14); otherwise tiles are dealt round-robin
+    const bool rowmap = G.NF8 / 8 == NWK && G.CTs == MAXT && !(a.debug & 8);
 #pragma unroll
     for (int s = 0; s < MAXT; ++s) {
-      const int t0 = w + s * NWK;
+      const int t0 = rowmap ? w * MAXT + s : w + s * NWK;
       const int t = min(t0, G.ntiles - 1);
       const int row = (t / G.CTs) * 8 + gid, c = (t % G.CTs) * 8 + 2 * tig;
       offY[s] = row * ldC + tig;
@@ -942,11 +946,22 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           if (!helper) {
             const double* Yp = Cr + jb;
             const double* Wp = T + (size_t)jb * ldT;
+            if (rowmap) {
 #pragma unroll
-            for (int k = 0; k < NB; k += 4) {
-              if (k < nk && !(a.debug & 2)) {
+              for (int k = 0; k < NB; k += 4) {
+                if (k < nk && !(a.debug & 2)) {
+                  const double y = -Yp[offY[0] + k];
 #pragma unroll
-                for (int s = 0; s < MAXT; ++s) dmma(acc[s], -Yp[offY[s] + k], Wp[offW[s] + k * ldT]);
+                  for (int s = 0; s < MAXT; ++s) dmma(acc[s], y, Wp[offW[s] + k * ldT]);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < NB; k += 4) {
+                if (k < nk && !(a.debug & 2)) {
+#pragma unroll
+                  for (int s = 0; s < MAXT; ++s) dmma(acc[s], -Yp[offY[s] + k], Wp[offW[s] + k * ldT]);
+                }
               }
             }
           }
