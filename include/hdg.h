@@ -126,7 +126,8 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* mesh, hdg_plan_info* info, hdg_
  * pivoting and form S_e = D_e - C_e A_e^-1 B_e, g_e = r_f - C_e A_e^-1 r_e.
  * Inputs A, B, C, D, r_e, r_f: packed as above (read only). Outputs S, g: packed. factors: opaque buffer of
  * plan.factor_bytes bytes holding the element factorizations for hdg_backsubstitute ("can be saved ... and
- * reused during the reconstruction"). info: int32 [n_elem]; info[l] = 0 on success, or k+1 if
+ * reused during the reconstruction"); its per-element records are 128-byte multiples, so a 128-byte
+ * aligned buffer (any cudaMalloc / torch allocation) keeps every record on whole DRAM atoms. info: int32 [n_elem]; info[l] = 0 on success, or k+1 if
  * the k-th pivot of element l was exactly zero, in which case S_l and g_l are set to NaN. */
 hdg_status hdg_condense(hdg_ctx ctx, const double* A, const double* B, const double* C, const double* D,
                         const double* r_e, const double* r_f, double* S, double* g, void* factors,

@@ -71,9 +71,12 @@ struct SweepGeo {
   }
 };
 
-// Opaque per-element factor record: [LU of P A_e, row-major, ne*ne doubles][perm: ne int32][pad to 16 B];
-// perm[i] = the row of A_e that is row i of P A_e.
-__host__ __device__ inline int64_t factor_bytes(int ne) { return ((int64_t)ne * ne * 8 + (int64_t)ne * 4 + 15) / 16 * 16; }
+// Opaque per-element factor record: [LU of P A_e, row-major, ne*ne doubles][perm: ne int32][pad to 128 B];
+// perm[i] = the row of A_e that is row i of P A_e. Records start on 128-byte boundaries (of a 128-byte aligned
+// buffer): with 16-byte padding every other C4 record (115,680 B) started 32 B into a 64-byte DRAM atom, so the
+// solves' 128-byte row segments touched three atoms instead of two (ncu: the adjoint kernels read 1.25x their
+// algorithmic bytes)
+__host__ __device__ inline int64_t factor_bytes(int ne) { return ((int64_t)ne * ne * 8 + (int64_t)ne * 4 + 127) / 128 * 128; }
 
 struct CondenseArgs {
   const double *A, *B, *C, *D, *re, *rf;
