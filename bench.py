@@ -121,7 +121,7 @@ def run_adjoint(args, wl, rank, world, local):
                        "step": "condense_adjoint_rhs + assemble_adjoint + backsubstitute_adjoint"},
             "adjoint_rhs_ms": rhs_ms, "assemble_adjoint_ms": asm_ms, "backsub_adjoint_ms": bs_ms,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                         "traffic": _traffic(args.config + "_adjoint_rhs"),
+                         "traffic": _traffic(args.config + "_adjoint_rhs") if args.degree is None else None,
                          "traffic_kernel": "adjoint_kernel<0> (dram read + write per launch, ncu --set full)",
                          "kernel": "adjoint_kernel<0, 1> (adjoint.cu)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs",
@@ -912,7 +912,9 @@ def main():
                     "frac": cond_gbs / (hbm or 6551.4), "traffic": None, "kernel": kname,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6551.4",
                     "bytes_per_launch": work["condense_bytes"], "fp64_tflops": cond_tflops}
-        roof["traffic"] = _traffic(args.config)
+        # (the stored capture is of the config's default kernel: none for another degree or a forced kernel)
+        default_kernel = args.degree is None and not os.environ.get("HDG_CONDENSE_KERNEL")
+        roof["traffic"] = _traffic(args.config) if default_kernel else None
         line = {
             "metric": METRIC, "value": elems / (ms_step * 1e-3), "unit": "elements/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

@@ -278,6 +278,16 @@ __device__ __forceinline__ bool prep_next(double* T, int ldT, int jb, int nb, in
   return viol;
 }
 
+// Row order of the accumulator tiles (and of their A operands) in the shared-memory updates: lane (gid, tig) of a
+// DMMA m8n8k4 holds accumulator row gid; if that row is T row gid, a 16-byte accumulator access (quarter warp =
+// rows gid, gid + 1) puts both rows in the same 64-byte half of the bank space for the row strides pad_ld picks
+// (4 or 12 mod 16 doubles, which keep the 8-byte fragment loads conflict-free) — 2-way conflicts on every
+// accumulator load and store (ncu: 30 % of the sweep kernel's shared wavefronts were conflict excess). Mapping
+// accumulator row g to T row srow(g) = g with bits 0 and 1 swapped (0, 2, 1, 3, 4, 6, 5, 7) makes the quarter-warp
+// row pairs (0, 2), (1, 3), ... land in opposite halves while the A fragments' 4-row phases keep 4 distinct bank
+// groups. The product is unchanged: A rows and accumulator rows are permuted together.
+__device__ __forceinline__ int srow(int g) { return (g & 4) | ((g & 1) << 1) | ((g >> 1) & 1); }
+
 // L21-type TRSM tile: rows r0..r0+8 of X (stride ld), columns jb..jb+nb: X <- X U11^-1. Returns whether any
 // multiplier |l| > 1 in a real (row < check_rows) position.
 // nrt (1 or 2) row tiles r0.. at once: 4 independent accumulator chains. When LU != nullptr the multipliers of
@@ -285,13 +295,14 @@ __device__ __forceinline__ bool prep_next(double* T, int ldT, int jb, int nb, in
 __device__ __forceinline__ bool trsm_right(double* X, int ld, int r0, int nrt, int jb, int nb, const double* Uinv,
                                            int check_rows, double* LU, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
+  const int sg = srow(gid);   // accumulator / A-operand row of this lane (bank-conflict-free row order)
   const int nk4 = (nb + 3) >> 2, nct = (nb + 7) >> 3;
   double a[2][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
-      a[i][kk] = (i < nrt && kk < nk4) ? X[(size_t)(r0 + 8 * i + gid) * ld + jb + 4 * kk + tig] : 0.0;
+      a[i][kk] = (i < nrt && kk < nk4) ? X[(size_t)(r0 + 8 * i + sg) * ld + jb + 4 * kk + tig] : 0.0;
   double acc[2][2][2] = {};
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
@@ -310,7 +321,7 @@ __device__ __forceinline__ bool trsm_right(double* X, int ld, int r0, int nrt, i
   bool viol = false;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const int row = r0 + 8 * i + gid;
+    const int row = r0 + 8 * i + sg;
     const bool chk = row < check_rows;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -332,6 +343,7 @@ __device__ __forceinline__ bool trsm_right(double* X, int ld, int r0, int nrt, i
 __device__ __forceinline__ void trsm_left(double* T, int ld, int jb, int nb, const double* Linv, int c0, int nct,
                                           double* LU, int ne, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
+  const int sg = srow(gid);   // accumulator / A-operand row of this lane (bank-conflict-free row order)
   const int nk4 = (nb + 3) >> 2, nrt = (nb + 7) >> 3;
   double b[4][2];
 #pragma unroll
@@ -343,7 +355,7 @@ __device__ __forceinline__ void trsm_left(double* T, int ld, int jb, int nb, con
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
     if (kk < nk4) {
-      const double l0 = Linv[gid * LDI + 4 * kk + tig], l1 = Linv[(8 + gid) * LDI + 4 * kk + tig];
+      const double l0 = Linv[sg * LDI + 4 * kk + tig], l1 = Linv[(8 + sg) * LDI + 4 * kk + tig];
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         if (j < nct) {
@@ -360,9 +372,9 @@ __device__ __forceinline__ void trsm_left(double* T, int ld, int jb, int nb, con
     for (int j = 0; j < 2; ++j)
       if (i < nrt && j < nct) {
         const int col = c0 + 8 * j + 2 * tig;
-        *reinterpret_cast<double2*>(T + (size_t)(jb + 8 * i + gid) * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
-        if (col < ne && 8 * i + gid < nb)
-          *reinterpret_cast<double2*>(LU + (size_t)(jb + 8 * i + gid) * ne + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+        *reinterpret_cast<double2*>(T + (size_t)(jb + 8 * i + sg) * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+        if (col < ne && 8 * i + sg < nb)
+          *reinterpret_cast<double2*>(LU + (size_t)(jb + 8 * i + sg) * ne + col) = make_double2(acc[i][j][0], acc[i][j][1]);
       }
 }
 
@@ -371,6 +383,7 @@ __device__ __forceinline__ void trsm_left(double* T, int ld, int jb, int nb, con
 __device__ __forceinline__ void upd_block(double* dst, int ldd, const double* Ap, int lda, const double* Bp, int ldb,
                                           int r0, int nrt, int c0, int nct, int nk, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
+  const int sg = srow(gid);   // accumulator / A-operand row of this lane (bank-conflict-free row order)
   double acc[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -379,7 +392,7 @@ __device__ __forceinline__ void upd_block(double* dst, int ldd, const double* Ap
       acc[i][j][0] = 0.0;
       acc[i][j][1] = 0.0;
       if (i < nrt && j < nct) {
-        const double2 v = *reinterpret_cast<const double2*>(dst + (size_t)(r0 + 8 * i + gid) * ldd + c0 + 8 * j + 2 * tig);
+        const double2 v = *reinterpret_cast<const double2*>(dst + (size_t)(r0 + 8 * i + sg) * ldd + c0 + 8 * j + 2 * tig);
         acc[i][j][0] = v.x;
         acc[i][j][1] = v.y;
       }
@@ -387,8 +400,8 @@ __device__ __forceinline__ void upd_block(double* dst, int ldd, const double* Ap
 #pragma unroll
   for (int k = 0; k < NB; k += 4) {
     if (k < nk) {
-      const double a0 = -Ap[(size_t)(r0 + gid) * lda + k + tig];
-      const double a1 = nrt > 1 ? -Ap[(size_t)(r0 + 8 + gid) * lda + k + tig] : 0.0;
+      const double a0 = -Ap[(size_t)(r0 + sg) * lda + k + tig];
+      const double a1 = nrt > 1 ? -Ap[(size_t)(r0 + 8 + sg) * lda + k + tig] : 0.0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (j < nct) {
@@ -404,7 +417,7 @@ __device__ __forceinline__ void upd_block(double* dst, int ldd, const double* Ap
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (i < nrt && j < nct)
-        *reinterpret_cast<double2*>(dst + (size_t)(r0 + 8 * i + gid) * ldd + c0 + 8 * j + 2 * tig) =
+        *reinterpret_cast<double2*>(dst + (size_t)(r0 + 8 * i + sg) * ldd + c0 + 8 * j + 2 * tig) =
             make_double2(acc[i][j][0], acc[i][j][1]);
 }
 
@@ -413,11 +426,12 @@ __device__ __forceinline__ void upd_block(double* dst, int ldd, const double* Ap
 __device__ __forceinline__ void upd_full16(double* dst, int ldd, const double* Ap, int lda, const double* Bp, int ldb,
                                            int r0, int c0, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
+  const int sg = srow(gid);   // accumulator / A-operand row of this lane (bank-conflict-free row order)
   double a[4][2], b[4][4];
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
-    a[kk][0] = -Ap[(size_t)(r0 + gid) * lda + 4 * kk + tig];
-    a[kk][1] = -Ap[(size_t)(r0 + 8 + gid) * lda + 4 * kk + tig];
+    a[kk][0] = -Ap[(size_t)(r0 + sg) * lda + 4 * kk + tig];
+    a[kk][1] = -Ap[(size_t)(r0 + 8 + sg) * lda + 4 * kk + tig];
 #pragma unroll
     for (int j = 0; j < 4; ++j) b[kk][j] = Bp[(size_t)(4 * kk + tig) * ldb + c0 + 8 * j + gid];
   }
@@ -426,7 +440,7 @@ __device__ __forceinline__ void upd_full16(double* dst, int ldd, const double* A
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const double2 v = *reinterpret_cast<const double2*>(dst + (size_t)(r0 + 8 * i + gid) * ldd + c0 + 8 * j + 2 * tig);
+      const double2 v = *reinterpret_cast<const double2*>(dst + (size_t)(r0 + 8 * i + sg) * ldd + c0 + 8 * j + 2 * tig);
       acc[i][j][0] = v.x;
       acc[i][j][1] = v.y;
     }
@@ -441,7 +455,7 @@ __device__ __forceinline__ void upd_full16(double* dst, int ldd, const double* A
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      *reinterpret_cast<double2*>(dst + (size_t)(r0 + 8 * i + gid) * ldd + c0 + 8 * j + 2 * tig) =
+      *reinterpret_cast<double2*>(dst + (size_t)(r0 + 8 * i + sg) * ldd + c0 + 8 * j + 2 * tig) =
           make_double2(acc[i][j][0], acc[i][j][1]);
 }
 
