@@ -48,6 +48,12 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// Row order of accumulator tiles and their A operands: accumulator row g <-> T row srow(g) (bits 0 and 1 of g
+// swapped), so the 16-byte accumulator accesses of a quarter warp (two rows) fall in opposite halves of the bank
+// space with the row stride Geo picks (4 mod 16 doubles, which keeps the 8-byte fragment loads conflict-free);
+// A rows and accumulator rows are permuted together, the product is unchanged (same fix as condense_sweep.cu).
+__device__ __forceinline__ int srow(int g) { return (g & 4) | ((g & 1) << 1) | ((g >> 1) & 1); }
+
 // dst[r][c] -= sum_{k < nk} As[r][k] * Bs[k][c] over rows [r_lo, r_hi) (multiples of 16) and columns
 // [c_lo, c_hi) (multiples of 8); nk multiple of 4. dst, As, Bs share the row stride ld. Work unit: a 16 x 32
 // block (2 x 4 tiles of 8x8) per warp, so each k-step loads 2 A- and 4 B-fragments for 8 DMMAs and every
@@ -60,7 +66,7 @@ __device__ __forceinline__ void mma_update(double* dst, const double* As, const 
   if (BR <= 0 || CT <= 0) return;
   const int BC = (CT + 3) >> 2;
   const int nblk = min(BR * BC, max_blocks);
-  const int gid = lane >> 2, tig = lane & 3;
+  const int gid = lane >> 2, tig = lane & 3, sg = srow(gid);
   for (int blk = first; blk < nblk; blk += stride) {
     const int br = blk / BC, bc = blk - br * BC;
     const int r0 = r_lo + br * 16, c0 = c_lo + bc * 32;
@@ -73,14 +79,14 @@ __device__ __forceinline__ void mma_update(double* dst, const double* As, const 
         acc[i][j][0] = 0.0;
         acc[i][j][1] = 0.0;
         if (j < nct) {
-          const double2 v = *reinterpret_cast<const double2*>(dst + (r0 + 8 * i + gid) * ld + c0 + 8 * j + 2 * tig);
+          const double2 v = *reinterpret_cast<const double2*>(dst + (r0 + 8 * i + sg) * ld + c0 + 8 * j + 2 * tig);
           acc[i][j][0] = v.x;
           acc[i][j][1] = v.y;
         }
       }
     for (int k = 0; k < nk; k += 4) {
-      const double a0 = -As[(r0 + gid) * ld + k + tig];
-      const double a1 = -As[(r0 + 8 + gid) * ld + k + tig];
+      const double a0 = -As[(r0 + sg) * ld + k + tig];
+      const double a1 = -As[(r0 + 8 + sg) * ld + k + tig];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (j < nct) {
@@ -95,7 +101,7 @@ __device__ __forceinline__ void mma_update(double* dst, const double* As, const 
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (j < nct)
-          *reinterpret_cast<double2*>(dst + (r0 + 8 * i + gid) * ld + c0 + 8 * j + 2 * tig) =
+          *reinterpret_cast<double2*>(dst + (r0 + 8 * i + sg) * ld + c0 + 8 * j + 2 * tig) =
               make_double2(acc[i][j][0], acc[i][j][1]);
   }
 }
@@ -254,23 +260,23 @@ __device__ __forceinline__ void diag_inverses(const double* T, int ldT, int jb, 
 // triangular (LOWER: L^-1, else U^-1): the MMAs with its exact-zero 8x8 quadrant are skipped.
 template <bool LOWER>
 __device__ __forceinline__ void inv_times_tile(double* T, int ldT, int jb, const double* Inv, int c0, int lane) {
-  const int gid = lane >> 2, tig = lane & 3;
+  const int gid = lane >> 2, tig = lane & 3, sg = srow(gid);
   double b[4];
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) b[kk] = T[(jb + 4 * kk + tig) * ldT + c0 + gid];
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
-    if (!LOWER || kk < 2) dmma(acc[0], Inv[gid * LDI + 4 * kk + tig], b[kk]);
-    if (LOWER || kk >= 2) dmma(acc[1], Inv[(8 + gid) * LDI + 4 * kk + tig], b[kk]);
+    if (!LOWER || kk < 2) dmma(acc[0], Inv[sg * LDI + 4 * kk + tig], b[kk]);
+    if (LOWER || kk >= 2) dmma(acc[1], Inv[(8 + sg) * LDI + 4 * kk + tig], b[kk]);
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i)
-    *reinterpret_cast<double2*>(T + (jb + 8 * i + gid) * ldT + c0 + 2 * tig) = make_double2(acc[i][0], acc[i][1]);
+    *reinterpret_cast<double2*>(T + (jb + 8 * i + sg) * ldT + c0 + 2 * tig) = make_double2(acc[i][0], acc[i][1]);
 }
 
 __device__ __forceinline__ void backsolve_tile(double* T, int ldT, int ne, const double* Uinv_all, int c0, int lane) {
-  const int gid = lane >> 2, tig = lane & 3;
+  const int gid = lane >> 2, tig = lane & 3, sg = srow(gid);
   const int npan = (ne + NB - 1) / NB;
   for (int p = npan - 1; p >= 0; --p) {
     const int jb = p * NB;
@@ -285,20 +291,20 @@ __device__ __forceinline__ void backsolve_tile(double* T, int ldT, int ne, const
       double acc[2][2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const double2 v = *reinterpret_cast<const double2*>(T + (r0 + 8 * i + gid) * ldT + c0 + 2 * tig);
+        const double2 v = *reinterpret_cast<const double2*>(T + (r0 + 8 * i + sg) * ldT + c0 + 2 * tig);
         acc[i][0] = v.x;
         acc[i][1] = v.y;
       }
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         if (kk < nk4) {
-          dmma(acc[0], -T[(r0 + gid) * ldT + jb + 4 * kk + tig], xb[kk]);
-          dmma(acc[1], -T[(r0 + 8 + gid) * ldT + jb + 4 * kk + tig], xb[kk]);
+          dmma(acc[0], -T[(r0 + sg) * ldT + jb + 4 * kk + tig], xb[kk]);
+          dmma(acc[1], -T[(r0 + 8 + sg) * ldT + jb + 4 * kk + tig], xb[kk]);
         }
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i)
-        *reinterpret_cast<double2*>(T + (r0 + 8 * i + gid) * ldT + c0 + 2 * tig) = make_double2(acc[i][0], acc[i][1]);
+        *reinterpret_cast<double2*>(T + (r0 + 8 * i + sg) * ldT + c0 + 2 * tig) = make_double2(acc[i][0], acc[i][1]);
     }
     __syncwarp();
   }
@@ -307,10 +313,10 @@ __device__ __forceinline__ void backsolve_tile(double* T, int ldT, int ne, const
 // T[r0..r0+8, jb..jb+16) <- T[r0..r0+8, jb..jb+16) * Uinv, in place (L21 = A21 U11^-1); one warp, one row tile.
 // Returns whether any multiplier exceeds 1 in magnitude (GEPP would have pivoted).
 __device__ __forceinline__ bool tile_times_uinv(double* T, int ldT, int jb, const double* Uinv, int r0, int lane) {
-  const int gid = lane >> 2, tig = lane & 3;
+  const int gid = lane >> 2, tig = lane & 3, sg = srow(gid);
   double a[4];
 #pragma unroll
-  for (int kk = 0; kk < 4; ++kk) a[kk] = T[(r0 + gid) * ldT + jb + 4 * kk + tig];
+  for (int kk = 0; kk < 4; ++kk) a[kk] = T[(r0 + sg) * ldT + jb + 4 * kk + tig];
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
@@ -321,7 +327,7 @@ __device__ __forceinline__ bool tile_times_uinv(double* T, int ldT, int jb, cons
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     viol |= fabs(acc[j][0]) > 1.0 || fabs(acc[j][1]) > 1.0;
-    *reinterpret_cast<double2*>(T + (r0 + gid) * ldT + jb + 8 * j + 2 * tig) = make_double2(acc[j][0], acc[j][1]);
+    *reinterpret_cast<double2*>(T + (r0 + sg) * ldT + jb + 8 * j + 2 * tig) = make_double2(acc[j][0], acc[j][1]);
   }
   return viol;
 }
