@@ -827,7 +827,6 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       if (lane == 0) v = atomicAdd(c, 1);
       return __shfl_sync(0xffffffffu, v, 0);
     };
-    const int hw_start = (w + NWK - 2) % NWK;   // static: regular TRSM jobs start from worker 2
     double acc[MAXT][2];
     // fixed shared-memory offsets of this worker's [S | g] tiles: Y rows (Cr) and W columns (T); slots past the
     // last tile accumulate into dead registers
@@ -942,7 +941,9 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           }
           // regular jobs start from worker 2: workers 0 and 1 (which also carry the look-ahead tiles) get the
           // remainder jobs last
-          for (int job = ((a.debug & 1) || helper) ? 1 << 30 : (GT ? claim(qctr + 2 + (pc & 1)) : hw_start);
+          // (measured: the helper taking regular jobs too in the first two thirds of the panels — 7 takers — made
+          //  C4 2.2 ms slower: its DMMAs on the chain warp's SMSP land during the chain's diagonal block)
+          for (int job = ((a.debug & 1) || helper) ? 1 << 30 : (GT ? claim(qctr + 2 + (pc & 1)) : (w + NWK - 2) % NWK);
                job < nA + nCt + nU; job = GT ? claim(qctr + 2 + (pc & 1)) : job + NWK) {
             if (job < nA) {
               viol |= trsm_right(T, ldT, rA0 + 16 * job, min(2, tA - 2 * job), jb, nb, Uinv, ne, LU, lane);
@@ -1002,7 +1003,10 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
               else { bi -= R1b.nblk; r_lo = R2.r_lo; r_hi = R2.r_hi; c_lo = R2.c_lo; c_hi = R2.c_hi; nbc = R2.nbc; }
               double* dst = inC ? Cr : T;
               const int ldd = inC ? ldC : ldT;
-              const int br = bi / nbc, bc = bi - br * nbc;
+              // block row by a fast float division ((bi + 0.5) / nbc is >= 1/16 from an integer for bi < 1024,
+              // nbc <= 8, far beyond __fdividef's error): ncu put 5 % of the stall samples on the integer division
+              // in front of every block's fragment loads (A/B in one binary: C4 condense 36.19 -> 35.39 ms)
+              const int br = (int)__fdividef((float)bi + 0.5f, (float)nbc), bc = bi - br * nbc;
               const int r0 = r_lo + 16 * br, c0 = c_lo + 32 * bc;
               const int nrt = min(2, (r_hi - r0) >> 3), nct = min(4, (c_hi - c0) >> 3);
               if (nrt == 2 && nct == 4 && NBC == NB) upd_full16(dst, ldd, dst + jb, ldd, T + (size_t)jb * ldT, ldT, r0, c0, lane);
