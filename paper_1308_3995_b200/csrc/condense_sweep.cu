@@ -94,7 +94,7 @@ __device__ __forceinline__ bool lu8(double* X, int ld, int r0, int nbv, double* 
   }
   if (r < nbv && j0 < nbv) {
     *reinterpret_cast<double2*>(X + (size_t)(r0 + r) * ld + r0 + j0) = make_double2(x0, x1);
-    *reinterpret_cast<double2*>(LU + (size_t)(r0 + r) * ne + r0 + j0) = make_double2(x0, x1);
+    st_cs2(LU + (size_t)(r0 + r) * ne + r0 + j0, x0, x1);
   }
   *reinterpret_cast<double2*>(stage + r * 8 + j0) = make_double2(x0, x1);
   __syncwarp();
@@ -160,11 +160,11 @@ __device__ __forceinline__ bool diag_chain(double* T, int ldT, int jb, int nb, d
     if (gid < n2) {
       viol |= fabs(l21[0]) > 1.0 || fabs(l21[1]) > 1.0;
       st8(D21, ldT, l21, lane);
-      *reinterpret_cast<double2*>(LU + (size_t)(jb + 8 + gid) * ne + jb + c) = make_double2(l21[0], l21[1]);
+      st_cs2(LU + (size_t)(jb + 8 + gid) * ne + jb + c, l21[0], l21[1]);
     }
     if (c < n2) {
       *reinterpret_cast<double2*>(D12 + gid * ldT + c) = make_double2(u12[0], u12[1]);
-      *reinterpret_cast<double2*>(LU + (size_t)(jb + gid) * ne + jb + 8 + c) = make_double2(u12[0], u12[1]);
+      st_cs2(LU + (size_t)(jb + gid) * ne + jb + 8 + c, u12[0], u12[1]);
     }
     __syncwarp();
     // D22 -= L21 U12 (entries of D22 outside the valid block are neither read nor written)
@@ -264,14 +264,14 @@ __device__ __forceinline__ bool prep_next(double* T, int ldT, int jb, int nb, in
         *reinterpret_cast<double2*>(T + (size_t)row * ldT + jb + c) = make_double2(accL[i][j][0], accL[i][j][1]);
         if (row < ne && c < nb) {
           viol |= fabs(accL[i][j][0]) > 1.0 || fabs(accL[i][j][1]) > 1.0;
-          *reinterpret_cast<double2*>(LU + (size_t)row * ne + jb + c) = make_double2(accL[i][j][0], accL[i][j][1]);
+          st_cs2(LU + (size_t)row * ne + jb + c, accL[i][j][0], accL[i][j][1]);
         }
       }
       if (i < nb8t && j < nctU) {
         const int row = jb + 8 * i + gid, col = jn + c;
         *reinterpret_cast<double2*>(T + (size_t)row * ldT + col) = make_double2(accU[i][j][0], accU[i][j][1]);
         if (8 * i + gid < nb && col < ne)
-          *reinterpret_cast<double2*>(LU + (size_t)row * ne + col) = make_double2(accU[i][j][0], accU[i][j][1]);
+          st_cs2(LU + (size_t)row * ne + col, accU[i][j][0], accU[i][j][1]);
       }
     }
   __syncwarp();
@@ -331,7 +331,7 @@ __device__ __forceinline__ bool trsm_right(double* X, int ld, int r0, int nrt, i
         if (chk && c + 1 < nb) viol |= fabs(acc[i][j][1]) > 1.0;
         *reinterpret_cast<double2*>(X + (size_t)row * ld + jb + c) = make_double2(acc[i][j][0], acc[i][j][1]);
         if (LU && chk && c < nb)
-          *reinterpret_cast<double2*>(LU + (size_t)row * check_rows + jb + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+          st_cs2(LU + (size_t)row * check_rows + jb + c, acc[i][j][0], acc[i][j][1]);
       }
     }
   }
@@ -374,7 +374,7 @@ __device__ __forceinline__ void trsm_left(double* T, int ld, int jb, int nb, con
         const int col = c0 + 8 * j + 2 * tig;
         *reinterpret_cast<double2*>(T + (size_t)(jb + 8 * i + sg) * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
         if (col < ne && 8 * i + sg < nb)
-          *reinterpret_cast<double2*>(LU + (size_t)(jb + 8 * i + sg) * ne + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+          st_cs2(LU + (size_t)(jb + 8 * i + sg) * ne + col, acc[i][j][0], acc[i][j][1]);
       }
 }
 
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     const double* sh = a.shift ? a.shift + a.offRe[l] : nullptr;
     for (int q = tid; q < ne * ha; q += THREADS) {
       const int i = q / ha, j = q - i * ha;
-      double2 v = __ldg(A + q);
+      double2 v = __ldcs(A + q);
       if (sh && (i >> 1) == j) {   // the diagonal entry of row i is in this pair
         if (i & 1) v.y += __ldg(sh + i);
         else v.x += __ldg(sh + i);
@@ -686,11 +686,11 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     }
     for (int q = tid; q < ne * hf; q += THREADS) {
       const int i = q / hf, j = q - i * hf;
-      *reinterpret_cast<double2*>(T + (size_t)i * ldT + CB + 2 * j) = __ldg(Bm + q);
+      *reinterpret_cast<double2*>(T + (size_t)i * ldT + CB + 2 * j) = __ldcs(Bm + q);
     }
     for (int q = tid; q < nf * ha; q += THREADS) {
       const int i = q / ha, j = q - i * ha;
-      *reinterpret_cast<double2*>(Cr + (size_t)i * ldC + 2 * j) = __ldg(Cm + q);
+      *reinterpret_cast<double2*>(Cr + (size_t)i * ldC + 2 * j) = __ldcs(Cm + q);
     }
   };
   // re-condensation: one warp adds element l's diagonal shift to rows [r_lo, r_hi) of T once they have landed
@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
 #pragma unroll
         for (int s = 0; s < MAXT; ++s) {
           const int o = offD[s];
-          const double2 v = __ldg(reinterpret_cast<const double2*>(D + (o >= 0 ? o : 0)));
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(D + (o >= 0 ? o : 0)));
           const double r0v = __ldg(rf + (o < -1 ? -o - 2 : 0));
           acc[s][0] = o >= 0 ? v.x : (o < -1 ? r0v : 0.0);
           acc[s][1] = o >= 0 ? v.y : 0.0;
@@ -906,6 +906,14 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         viol = false;
         // the next panel's counters: their last users (the previous panel) have all passed the barrier above
         if (GT && helper && lane == 0) qctr[(pc + 1) & 1] = qctr[2 + ((pc + 1) & 1)] = 0;
+        if (GT && helper && p >= 1 && !(a.debug & 16)) {
+          // the slab rows of panel p-1 are dead for the rest of the element (their L\U is in the factor record,
+          // their U12 / W parts were last read by panel p-1's updates): drop their L2 lines without a write-back
+          // (only lines entirely inside those rows; the next element's staging rewrites them)
+          const uintptr_t lo = ((uintptr_t)(T + (size_t)(p - 1) * NB * ldT) + 127) & ~(uintptr_t)127;
+          const uintptr_t hi = (uintptr_t)(T + (size_t)min(p * NB, ne) * ldT) & ~(uintptr_t)127;
+          for (uintptr_t q = lo + 128 * (uintptr_t)lane; q < hi; q += 128 * 32) discard_l2_line((const void*)q);
+        }
         if (!GT && helper && p >= 1 && ln >= 0) {
           // the rows of panel p-1 are dead: stream the next element's rows in
           if (p == 1) expect_all();
@@ -1066,7 +1074,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
 #pragma unroll
             for (int s = 0; s < MAXT; ++s) {
               const int o = offD[s];
-              if (o >= 0) *reinterpret_cast<double2*>(S + o) = make_double2(acc[s][0], acc[s][1]);
+              if (o >= 0) st_cs2(S + o, acc[s][0], acc[s][1]);
               else if (o < -1) g[-o - 2] = acc[s][0];
             }
           }

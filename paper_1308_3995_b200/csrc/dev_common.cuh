@@ -32,6 +32,15 @@ __device__ __forceinline__ double rcp_fast(double x) {
   return fma(r, t, r);
 }
 
+// streaming (evict-first) 16-byte global store: factor records and S are written once and not re-read by this
+// kernel, so they should not displace L2-resident working data (the GT sweep's slabs)
+__device__ __forceinline__ void st_cs2(double* p, double x, double y) {
+  __stcs(reinterpret_cast<double2*>(p), make_double2(x, y));
+}
+// drop one 128-byte L2 line of dead global data without writing it back (its contents become undefined)
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
