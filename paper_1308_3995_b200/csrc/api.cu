@@ -340,15 +340,17 @@ hdg_status hdg_plan(hdg_ctx ctx, const hdg_mesh* m, hdg_plan_info* info, hdg_str
     const Geo geo(B.ne, B.nf);
     B.t_in_smem = geo.smem_bytes(true) <= (int64_t)ctx->smem_optin;
     // measured on the box: the sweep kernel (chain warp + MMA workers; 2 CTAs per SM when they fit) wins for
-    // n_e >= 96 (C4: 45 vs 57 ms) and n_e <= 32 (C2: 0.82 vs 0.95 ms); the panel kernel for n_e in between
-    // (C3: 34 vs 40 ms)
+    // n_e >= 96 (C4: 45 vs 57 ms), for C5's n_e = 72 buckets (C5 slab 85.0 -> 81.6 ms vs the panel kernel) and
+    // n_e <= 32 (C2: 0.82 vs 0.95 ms); the panel kernel for n_e = 60 (C3: 34 vs 40 ms). The (120, n_f > 48)
+    // buckets, whose C rows do not fit beside T, stay on the panel kernel (the GT sweep measured 85.0 -> 87.5 ms)
     const char* forced = getenv("HDG_CONDENSE_KERNEL");
     const std::string fk = forced ? forced : "";
     // small elements (C1, C2): one warp per element, 16+ elements in flight per SM (C2: 0.71 ms on the sweep
     // kernel, see DESIGN §11 for the warp kernel's number); HDG_CONDENSE_KERNEL=sweep|panel force the others
     B.warp = warp_supported(B.ne, B.nf) && fk != "sweep" && fk != "panel";
+    const int sweep_min = getenv("HDG_SWEEP_MIN_NE") ? atoi(getenv("HDG_SWEEP_MIN_NE")) : 64;   // experiments
     B.sweep = !B.warp && sweep_supported(B.ne, B.nf, ctx->smem_optin) && fk != "panel" &&
-              (B.ne >= 96 || B.ne <= 32 || fk == "sweep");
+              (B.ne >= sweep_min || B.ne <= 32 || fk == "sweep");
     // the row-tile kernel (condense_rows.cu): HDG_CONDENSE_KERNEL=rows
     B.rows = !B.warp && fk == "rows" && rows_supported(B.ne, B.nf, ctx->smem_optin);
     if (B.rows) B.sweep = false;

@@ -110,6 +110,14 @@ def test_gt_sweep_p4_p5_480_elements(cuda, p):
     check_perturbed(w, seed=500 + p)
 
 
+def test_ns_p2_sweep_960_elements(cuda):
+    """NS p = 2 (n_e = 72, n_f = 36: C5's n_e = 72 buckets, on the shared-memory sweep kernel since session 4 of
+    round 2, two CTAs per SM when they fit): 960 elements -> >= 3 per CTA."""
+    w = gen.make_workload("NSp2", nr=20, nt=24, m_elem=12, p_fixed=2, seed=gen.SEED_BASE + 6)
+    assert int(w.elem_ne[0]) == 72 and w.E >= 3 * 296
+    check_perturbed(w, seed=602)
+
+
 def test_c2_sized_7200_elements(cuda):
     """n_e = 24, n_f = 36 (C2 blocks, the warp-per-element kernel): 7200 elements -> >= 3 per warp slot at 16
     warps per SM."""
