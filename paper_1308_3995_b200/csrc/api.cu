@@ -564,11 +564,29 @@ static hdg_status condense_impl(hdg_ctx ctx, const double* A, const double* B, c
     const bool forms_x = b.warp || (!b.rows && !b.sweep && !b.sweep_gt);
     a.Xout = (X && forms_x) ? X : nullptr;
     a.offX = p.d_off[OFF_X];
+    // diagnostics: HDG_BUCKET_TIMES=1 prints each bucket's kernel time (synchronizes; never in a timed run)
+    static const bool bucket_times = getenv("HDG_BUCKET_TIMES") != nullptr;
+    cudaEvent_t bt0 = nullptr, bt1 = nullptr;
+    if (bucket_times) {
+      cudaEventCreate(&bt0);
+      cudaEventCreate(&bt1);
+      cudaEventRecord(bt0, s);
+    }
     if (b.warp) HDG_CUDA(ctx, launch_condense_warp(a, ctx->sms, s, &ctx->launches));
     else if (b.rows) HDG_CUDA(ctx, launch_condense_rows(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
     else if (b.sweep) HDG_CUDA(ctx, launch_condense_sweep(a, ctx->sms, ctx->smem_optin, s, &ctx->launches));
     else if (b.sweep_gt) HDG_CUDA(ctx, launch_condense_sweep_gt(a, ctx->sms, s, &ctx->launches));
     else HDG_CUDA(ctx, launch_condense(a, b.t_in_smem, ctx->sms, s, &ctx->launches));
+    if (bucket_times) {
+      float ms = 0.f;
+      cudaEventRecord(bt1, s);
+      cudaEventSynchronize(bt1);
+      cudaEventElapsedTime(&ms, bt0, bt1);
+      fprintf(stderr, "HDG_BUCKET_TIMES ne %d nf %d count %lld kernel %s ms %.3f\n", b.ne, b.nf, (long long)b.count,
+              b.warp ? "warp" : b.rows ? "rows" : b.sweep ? "sweep" : b.sweep_gt ? "sweep_gt" : "panel", ms);
+      cudaEventDestroy(bt0);
+      cudaEventDestroy(bt1);
+    }
     if (X && !forms_x) {
       SolutionsArgs q{};
       q.factors = a.factors; q.B = B; q.re = r_e; q.X = X;
