@@ -58,6 +58,7 @@ constexpr int BCW = 36;   // doubles per spare chain-warp slot (two slots: the 8
 // shared-memory copy of L\U (stage, 64 doubles): lanes 0-7 column j of L^-1, lanes 8-15 column j of U^-1 through
 // the reversal J U J (lower triangular), with the pivot reciprocals kept from the elimination. Writes L\U rows
 // < nbv back to X and to LU.
+template <bool CS>
 __device__ __forceinline__ bool lu8(double* X, int ld, int r0, int nbv, double* Li8, double* Ui8, double* LU, int ne,
                                     double* stage, int lane) {
   __syncwarp();
@@ -94,7 +95,7 @@ __device__ __forceinline__ bool lu8(double* X, int ld, int r0, int nbv, double* 
   }
   if (r < nbv && j0 < nbv) {
     *reinterpret_cast<double2*>(X + (size_t)(r0 + r) * ld + r0 + j0) = make_double2(x0, x1);
-    st_cs2(LU + (size_t)(r0 + r) * ne + r0 + j0, x0, x1);
+    st_lu<CS>(LU + (size_t)(r0 + r) * ne + r0 + j0, x0, x1);
   }
   *reinterpret_cast<double2*>(stage + r * 8 + j0) = make_double2(x0, x1);
   __syncwarp();
@@ -142,11 +143,12 @@ __device__ __forceinline__ void st8(double* D, int ld, const double (&acc)[2], i
 // Same pivot order and GEPP check as a 16-step elimination (every multiplier |l| <= 1, pivots normal), with
 // half the broadcast traffic per step and a quarter of the code (measured on the box: the fully unrolled 16-step
 // body spends ~2x its standalone time in the kernel, instruction fetch). L\U goes to T and the factor record LU.
+template <bool CS>
 __device__ __forceinline__ bool diag_chain(double* T, int ldT, int jb, int nb, double* Linv, double* Uinv,
                                            double* stage, double* LU, int ne, int lane) {
   __syncwarp();
   const int n1 = nb < 8 ? nb : 8, n2 = nb > 8 ? nb - 8 : 0;
-  bool viol = lu8(T, ldT, jb, n1, Linv, Uinv, LU, ne, stage, lane);
+  bool viol = lu8<CS>(T, ldT, jb, n1, Linv, Uinv, LU, ne, stage, lane);
   const int gid = lane >> 2, tig = lane & 3, c = 2 * tig;
   double* D12 = T + (size_t)jb * ldT + jb + 8;
   double* D21 = T + (size_t)(jb + 8) * ldT + jb;
@@ -160,11 +162,11 @@ __device__ __forceinline__ bool diag_chain(double* T, int ldT, int jb, int nb, d
     if (gid < n2) {
       viol |= fabs(l21[0]) > 1.0 || fabs(l21[1]) > 1.0;
       st8(D21, ldT, l21, lane);
-      st_cs2(LU + (size_t)(jb + 8 + gid) * ne + jb + c, l21[0], l21[1]);
+      st_lu<CS>(LU + (size_t)(jb + 8 + gid) * ne + jb + c, l21[0], l21[1]);
     }
     if (c < n2) {
       *reinterpret_cast<double2*>(D12 + gid * ldT + c) = make_double2(u12[0], u12[1]);
-      st_cs2(LU + (size_t)(jb + gid) * ne + jb + 8 + c, u12[0], u12[1]);
+      st_lu<CS>(LU + (size_t)(jb + gid) * ne + jb + 8 + c, u12[0], u12[1]);
     }
     __syncwarp();
     // D22 -= L21 U12 (entries of D22 outside the valid block are neither read nor written)
@@ -176,7 +178,7 @@ __device__ __forceinline__ bool diag_chain(double* T, int ldT, int jb, int nb, d
     if (gid < n2 && c < n2) *reinterpret_cast<double2*>(D22 + gid * ldT + c) = make_double2(d22[0], d22[1]);
     __syncwarp();
   }
-  viol |= lu8(T, ldT, jb + 8, n2, Linv + 8 * LDI + 8, Uinv + 8 * LDI + 8, LU, ne, stage, lane);
+  viol |= lu8<CS>(T, ldT, jb + 8, n2, Linv + 8 * LDI + 8, Uinv + 8 * LDI + 8, LU, ne, stage, lane);
   // off-diagonal tiles of the inverses: stage P = L21 L1^-1 and Q = U12 U2^-1 in their final tiles, then
   // X = -L2^-1 P, Y = -U1^-1 Q; zero the other off-diagonal tiles
   double P[2] = {0.0, 0.0}, Q[2] = {0.0, 0.0};
@@ -201,13 +203,14 @@ __device__ __forceinline__ bool diag_chain(double* T, int ldT, int jb, int nb, d
 
 // The diagonal block of one panel: NB = 8 -> one 8x8 LU (its L^-1, U^-1 written straight into the Linv / Uinv
 // buffers); NB = 16 -> the two-LU form above.
+template <bool CS>
 __device__ __forceinline__ bool diag_block(double* T, int ldT, int jb, int nb, double* Linv, double* Uinv,
                                            double* scratch, double* LU, int ne, int lane) {
   if constexpr (NB == 8) {
     __syncwarp();
-    return lu8(T, ldT, jb, nb, Linv, Uinv, LU, ne, scratch, lane);
+    return lu8<CS>(T, ldT, jb, nb, Linv, Uinv, LU, ne, scratch, lane);
   } else {
-    return diag_chain(T, ldT, jb, nb, Linv, Uinv, scratch, LU, ne, lane);
+    return diag_chain<CS>(T, ldT, jb, nb, Linv, Uinv, scratch, LU, ne, lane);
   }
 }
 
@@ -215,6 +218,7 @@ __device__ __forceinline__ bool diag_block(double* T, int ldT, int jb, int nb, d
 // prep_next (chain warp): the L21 rows [jn, r_hi) and U12 columns [jn, jn + nn8) of the NEXT diagonal block from
 // panel (jb, nb), all 8 accumulator chains interleaved, stored to T (and the factor record), then that block's
 // update D_{p+1} -= L21 U12. Returns whether a multiplier |l| > 1 appeared.
+template <bool CS>
 __device__ __forceinline__ bool prep_next(double* T, int ldT, int jb, int nb, int jn, int r_hi, int nn8,
                                           const double* Linv, const double* Uinv, double* LU, int ne, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
@@ -264,14 +268,14 @@ __device__ __forceinline__ bool prep_next(double* T, int ldT, int jb, int nb, in
         *reinterpret_cast<double2*>(T + (size_t)row * ldT + jb + c) = make_double2(accL[i][j][0], accL[i][j][1]);
         if (row < ne && c < nb) {
           viol |= fabs(accL[i][j][0]) > 1.0 || fabs(accL[i][j][1]) > 1.0;
-          st_cs2(LU + (size_t)row * ne + jb + c, accL[i][j][0], accL[i][j][1]);
+          st_lu<CS>(LU + (size_t)row * ne + jb + c, accL[i][j][0], accL[i][j][1]);
         }
       }
       if (i < nb8t && j < nctU) {
         const int row = jb + 8 * i + gid, col = jn + c;
         *reinterpret_cast<double2*>(T + (size_t)row * ldT + col) = make_double2(accU[i][j][0], accU[i][j][1]);
         if (8 * i + gid < nb && col < ne)
-          st_cs2(LU + (size_t)row * ne + col, accU[i][j][0], accU[i][j][1]);
+          st_lu<CS>(LU + (size_t)row * ne + col, accU[i][j][0], accU[i][j][1]);
       }
     }
   __syncwarp();
@@ -292,6 +296,7 @@ __device__ __forceinline__ int srow(int g) { return (g & 4) | ((g & 1) << 1) | (
 // multiplier |l| > 1 in a real (row < check_rows) position.
 // nrt (1 or 2) row tiles r0.. at once: 4 independent accumulator chains. When LU != nullptr the multipliers of
 // real rows (< check_rows = ne) are also stored to the factor record.
+template <bool CS>
 __device__ __forceinline__ bool trsm_right(double* X, int ld, int r0, int nrt, int jb, int nb, const double* Uinv,
                                            int check_rows, double* LU, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
@@ -331,7 +336,7 @@ __device__ __forceinline__ bool trsm_right(double* X, int ld, int r0, int nrt, i
         if (chk && c + 1 < nb) viol |= fabs(acc[i][j][1]) > 1.0;
         *reinterpret_cast<double2*>(X + (size_t)row * ld + jb + c) = make_double2(acc[i][j][0], acc[i][j][1]);
         if (LU && chk && c < nb)
-          st_cs2(LU + (size_t)row * check_rows + jb + c, acc[i][j][0], acc[i][j][1]);
+          st_lu<CS>(LU + (size_t)row * check_rows + jb + c, acc[i][j][0], acc[i][j][1]);
       }
     }
   }
@@ -340,6 +345,7 @@ __device__ __forceinline__ bool trsm_right(double* X, int ld, int r0, int nrt, i
 
 // U12-type TRSM tile: rows jb..jb+nb (rounded up to 8) of T, columns c0..c0+8: T <- L11^-1 T. Columns < ne are
 // U entries and are also stored to the factor record LU (row stride ne).
+template <bool CS>
 __device__ __forceinline__ void trsm_left(double* T, int ld, int jb, int nb, const double* Linv, int c0, int nct,
                                           double* LU, int ne, int lane) {
   const int gid = lane >> 2, tig = lane & 3;
@@ -374,7 +380,7 @@ __device__ __forceinline__ void trsm_left(double* T, int ld, int jb, int nb, con
         const int col = c0 + 8 * j + 2 * tig;
         *reinterpret_cast<double2*>(T + (size_t)(jb + 8 * i + sg) * ld + col) = make_double2(acc[i][j][0], acc[i][j][1]);
         if (col < ne && 8 * i + sg < nb)
-          st_cs2(LU + (size_t)(jb + 8 * i + sg) * ne + col, acc[i][j][0], acc[i][j][1]);
+          st_lu<CS>(LU + (size_t)(jb + 8 * i + sg) * ne + col, acc[i][j][0], acc[i][j][1]);
       }
 }
 
@@ -677,7 +683,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     const double* sh = a.shift ? a.shift + a.offRe[l] : nullptr;
     for (int q = tid; q < ne * ha; q += THREADS) {
       const int i = q / ha, j = q - i * ha;
-      double2 v = __ldcs(A + q);
+      double2 v = __ldg(A + q);
       if (sh && (i >> 1) == j) {   // the diagonal entry of row i is in this pair
         if (i & 1) v.y += __ldg(sh + i);
         else v.x += __ldg(sh + i);
@@ -686,11 +692,11 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
     }
     for (int q = tid; q < ne * hf; q += THREADS) {
       const int i = q / hf, j = q - i * hf;
-      *reinterpret_cast<double2*>(T + (size_t)i * ldT + CB + 2 * j) = __ldcs(Bm + q);
+      *reinterpret_cast<double2*>(T + (size_t)i * ldT + CB + 2 * j) = __ldg(Bm + q);
     }
     for (int q = tid; q < nf * ha; q += THREADS) {
       const int i = q / ha, j = q - i * ha;
-      *reinterpret_cast<double2*>(Cr + (size_t)i * ldC + 2 * j) = __ldcs(Cm + q);
+      *reinterpret_cast<double2*>(Cr + (size_t)i * ldC + 2 * j) = __ldg(Cm + q);
     }
   };
   // re-condensation: one warp adds element l's diagonal shift to rows [r_lo, r_hi) of T once they have landed
@@ -780,7 +786,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           SW_STAMP(tit, 10 + 4 * p);
         }
         if (do_diag)
-          viol |= diag_block(T, ldT, jd, nd, Linv_b + dbuf * NB * LDI, Uinv_b + dbuf * NB * LDI, bcast, LUd, ne, lane);
+          viol |= diag_block<GT>(T, ldT, jd, nd, Linv_b + dbuf * NB * LDI, Uinv_b + dbuf * NB * LDI, bcast, LUd, ne, lane);
         if (p < 0) {
           SW_STAMP(tit, 2);
           if (!GT) mbar_wait(&mbar[1], ph);
@@ -883,7 +889,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
 #pragma unroll
         for (int s = 0; s < MAXT; ++s) {
           const int o = offD[s];
-          const double2 v = __ldcs(reinterpret_cast<const double2*>(D + (o >= 0 ? o : 0)));
+          const double2 v = __ldg(reinterpret_cast<const double2*>(D + (o >= 0 ? o : 0)));
           const double r0v = __ldg(rf + (o < -1 ? -o - 2 : 0));
           acc[s][0] = o >= 0 ? v.x : (o < -1 ? r0v : 0.0);
           acc[s][1] = o >= 0 ? v.y : 0.0;
@@ -942,8 +948,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           const int nA = (tA + 1) >> 1, nCt = (tC + 1) >> 1, nU = (tU + 1) >> 1;
           if (has_next && w < 2 && !helper) {
             // the tiles the chain warp's next diagonal block needs, first: L21 of its rows, U12 of its columns
-            if (w == 0) viol |= trsm_right(T, ldT, jn, (nextr_hi - jn) >> 3, jb, nb, Uinv, ne, LU, lane);
-            else trsm_left(T, ldT, jb, nb, Linv, jn, nn8 >> 3, LU, ne, lane);
+            if (w == 0) viol |= trsm_right<GT>(T, ldT, jn, (nextr_hi - jn) >> 3, jb, nb, Uinv, ne, LU, lane);
+            else trsm_left<GT>(T, ldT, jb, nb, Linv, jn, nn8 >> 3, LU, ne, lane);
             __syncwarp();
             named_arrive(2, 96);
           }
@@ -954,13 +960,13 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           for (int job = ((a.debug & 1) || helper) ? 1 << 30 : (GT ? claim(qctr + 2 + (pc & 1)) : (w + NWK - 2) % NWK);
                job < nA + nCt + nU; job = GT ? claim(qctr + 2 + (pc & 1)) : job + NWK) {
             if (job < nA) {
-              viol |= trsm_right(T, ldT, rA0 + 16 * job, min(2, tA - 2 * job), jb, nb, Uinv, ne, LU, lane);
+              viol |= trsm_right<GT>(T, ldT, rA0 + 16 * job, min(2, tA - 2 * job), jb, nb, Uinv, ne, LU, lane);
             } else if (job < nA + nCt) {
               const int q = job - nA;
-              trsm_right(Cr, ldC, 16 * q, min(2, tC - 2 * q), jb, nb, Uinv, 0, nullptr, lane);
+              trsm_right<GT>(Cr, ldC, 16 * q, min(2, tC - 2 * q), jb, nb, Uinv, 0, nullptr, lane);
             } else {
               const int q = job - nA - nCt;
-              trsm_left(T, ldT, jb, nb, Linv, cU0 + 16 * q, min(2, tU - 2 * q), LU, ne, lane);
+              trsm_left<GT>(T, ldT, jb, nb, Linv, cU0 + 16 * q, min(2, tU - 2 * q), LU, ne, lane);
             }
           }
           named_sync(1, THREADS);
@@ -1074,7 +1080,7 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
 #pragma unroll
             for (int s = 0; s < MAXT; ++s) {
               const int o = offD[s];
-              if (o >= 0) st_cs2(S + o, acc[s][0], acc[s][1]);
+              if (o >= 0) st_lu<GT>(S + o, acc[s][0], acc[s][1]);
               else if (o < -1) g[-o - 2] = acc[s][0];
             }
           }

@@ -32,10 +32,13 @@ __device__ __forceinline__ double rcp_fast(double x) {
   return fma(r, t, r);
 }
 
-// streaming (evict-first) 16-byte global store: factor records and S are written once and not re-read by this
-// kernel, so they should not displace L2-resident working data (the GT sweep's slabs)
-__device__ __forceinline__ void st_cs2(double* p, double x, double y) {
-  __stcs(reinterpret_cast<double2*>(p), make_double2(x, y));
+// 16-byte global store of a factor-record / S entry: streaming (st.global.cs, evict-first) when CS — the GT sweep,
+// whose working slabs live in L2 and must not be displaced by write-once data (C4 mesh at p = 4: 129.3 -> 125.0 ms,
+// C5 slab 81.3 -> 77.8 ms) — plain otherwise (the shared-memory sweep measured 35.2 vs 35.5 ms with .cs)
+template <bool CS>
+__device__ __forceinline__ void st_lu(double* p, double x, double y) {
+  if constexpr (CS) __stcs(reinterpret_cast<double2*>(p), make_double2(x, y));
+  else *reinterpret_cast<double2*>(p) = make_double2(x, y);
 }
 // drop one 128-byte L2 line of dead global data without writing it back (its contents become undefined)
 __device__ __forceinline__ void discard_l2_line(const void* p) {
