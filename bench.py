@@ -161,14 +161,14 @@ def run_solve(args, wl, rank, world, local):
         if timed:
             res.append(([ev[i].elapsed_time(ev[i + 1]) for i in range(4)], it, rr))
 
+    clocks = ClockSampler(local)
+    clocks.start()                       # before the warm-up: nvidia-smi needs 0.1-0.3 s for its first sample
     for _ in range(args.warmup):
         step(False)
-    clocks = ClockSampler(local)
-    clocks.start()
     clocks.mark()
     for _ in range(args.steps):
         step(True)
-    clk = clocks.stop()
+    clk = clocks.stop(replay=lambda: step(False))
     # one SpMV alone (HBM rate of the solver's dominant kernel)
     a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     x = torch.randn(w.n_trace, dtype=torch.float64, device=lam.device)
