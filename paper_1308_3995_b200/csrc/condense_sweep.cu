@@ -47,6 +47,7 @@ constexpr int NB = kSweepNB;   // panel width (see diag_block for NB = 8 / 16)
   } while (0)
 constexpr int LDI = 20;   // row stride of the 16x16 inverse buffers
 
+constexpr int kHelperShare = 14;   // 64ths of a panel's trailing blocks taken by the helper warp (see the trailing loop)
 constexpr int BCW = 36;   // doubles per spare chain-warp slot (two slots: the 8x8 LU's staging copy)
 
 // ------------------------------------------------------------------------------------------------------------
@@ -956,7 +957,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
           // regular jobs start from worker 2: workers 0 and 1 (which also carry the look-ahead tiles) get the
           // remainder jobs last
           // (measured: the helper taking regular jobs too in the first two thirds of the panels — 7 takers — made
-          //  C4 2.2 ms slower: its DMMAs on the chain warp's SMSP land during the chain's diagonal block)
+          //  C4 2.2 ms slower: its DMMAs on the chain warp's SMSP land during the chain's diagonal block; re-measured
+          //  with the helper's own trailing share, its last 1-3 jobs in the first 2-6 panels only: 34.3-36.0 vs 34.05 ms)
           for (int job = ((a.debug & 1) || helper) ? 1 << 30 : (GT ? claim(qctr + 2 + (pc & 1)) : (w + NWK - 2) % NWK);
                job < nA + nCt + nU; job = GT ? claim(qctr + 2 + (pc & 1)) : job + NWK) {
             if (job < nA) {
@@ -1007,8 +1009,21 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
             const bool hjoin = 3 * p < 2 * G.npan;   // (first 2/3: C4 38.7 -> 38.4 ms vs the first half)
             const int nt_w = hjoin ? NWK + 1 : NWK;
             const int tw = helper ? NWK : w;
-            for (int b = ((a.debug & 1) || (helper && !hjoin)) ? 1 << 30 : (GT ? claim(qctr + (pc & 1)) : tw); b < tot;
-                 b = GT ? claim(qctr + (pc & 1)) : b + nt_w) {
+            // Shared-memory T: the helper takes the LAST kHelperShare/64 of the blocks one after another (mostly the
+            // C-row blocks of R2, starting while the workers still update [S | g]) and the workers deal the rest
+            // round-robin. Measured on C4 in
+            // one binary (HDG_DEBUG_MODE bits 8-13 override the share; 1 = the previous 7-taker interleaved deal):
+            // interleaved 35.1-35.3 ms, share 10: 35.0, 12: 34.4, 13: 34.3, 14: 34.0-34.4, 15: 34.4, 16: 35.7,
+            // 18: 37.6 ms; joining in more or fewer panels, or rounding the workers' share to whole rounds: no gain.
+            // (Also measured, not adopted: the C rows on an mbarrier of their own, waited for at their first use in
+            // panel 0 with the Y_p jobs dealt last — 34.5-34.7 vs 34.05 ms: the element start is not bound by them.)
+            const int hsel = ((a.debug >> 8) & 63) ? (a.debug >> 8) & 63 : kHelperShare;
+            const int nh = (!GT && hjoin && hsel > 1) ? (tot * hsel) >> 6 : -1;
+            const int b_end = (nh >= 0 && !helper) ? tot - nh : tot;
+            const int b0 = nh >= 0 ? (helper ? tot - nh : w) : tw;
+            const int bs = nh >= 0 ? (helper ? 1 : NWK) : nt_w;
+            for (int b = ((a.debug & 1) || (helper && !hjoin)) ? 1 << 30 : (GT ? claim(qctr + (pc & 1)) : b0); b < b_end;
+                 b = GT ? claim(qctr + (pc & 1)) : b + bs) {
               // region selection with plain integers (no addresses of locals: they would live on the stack)
               int bi = b, r_lo, r_hi, c_lo, c_hi, nbc;
               const bool inC = bi >= R1a.nblk + R1b.nblk;

@@ -20,7 +20,7 @@ timeout 900 $NCU -k regex:adjoint_kernel -c 2 -o $O/adjoint_C4 -f python bench.p
 timeout 300 python bench.py --config C4 --path saved --steps 1 --warmup 1 $Q > $O/plain_saved.log 2>&1 && \
 timeout 900 $NCU -k regex:"backsub_saved_kernel|save_kernel" -c 2 -o $O/saved_C4 -f python bench.py --config C4 --path saved --steps 1 --warmup 1 $Q > $O/ncu_saved.log 2>&1
 timeout 300 python bench.py --config C5 --slab 0/8 --steps 1 --warmup 1 $Q > $O/plain_c5.log 2>&1 && \
-timeout 1200 $NCU -k regex:"sweep_kernel<16" -c 2 -o $O/gt_C5 -f python bench.py --config C5 --slab 0/8 --steps 1 --warmup 1 $Q > $O/ncu_gt.log 2>&1
+timeout 1200 $NCU -k regex:"sweep_kernel<.int.16" -c 2 -o $O/gt_C5 -f python bench.py --config C5 --slab 0/8 --steps 1 --warmup 1 $Q > $O/ncu_gt.log 2>&1
 R=""; add() { [ -f $O/$1.ncu-rep ] && R="$R --rep $O/$1.ncu-rep --config $2 --kernel $3"; }
 add sweep_C4 C4 sweep_kernel; add backsub_C4 C4 backsub_kernel; add panel_C3 C3 condense_kernel; add warp_C2 C2 warp_kernel
 add adjoint_C4 C4rhs "adjoint_kernel<0>"; add adjoint_C4 C4recon "adjoint_kernel<1>"
