@@ -853,7 +853,20 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
       offD[s] = (t0 < G.ntiles && row < nf) ? (c < nf ? row * nf + c : (c == nf ? -(row + 2) : -1)) : -1;
     }
     double rv[(kMaxNe + 31) / 32];   // helper: the next element's r_e column, loaded ahead
-    bool have_rv = false;
+    bool have_rv = false, have_acc = false;
+    // the accumulators from D_e / r_f (precomputed offsets: no divisions, no branches around the loads)
+    auto load_acc = [&](int64_t le) {
+      const double* D = a.D + a.offD[le];
+      const double* rf = a.rf + a.offRf[le];
+#pragma unroll
+      for (int s = 0; s < MAXT; ++s) {
+        const int o = offD[s];
+        const double2 v = __ldg(reinterpret_cast<const double2*>(D + (o >= 0 ? o : 0)));
+        const double r0v = __ldg(rf + (o < -1 ? -o - 2 : 0));
+        acc[s][0] = o >= 0 ? v.x : (o < -1 ? r0v : 0.0);
+        acc[s][1] = o >= 0 ? v.y : 0.0;
+      }
+    };
     for (int64_t it = blockIdx.x; it < a.count; it += gridDim.x, ph ^= 1u) {
       const int64_t l = elem_of(it);
       const int64_t next = it + gridDim.x;
@@ -884,17 +897,8 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
         for (int q = 0; q < (kMaxNe + 31) / 32; ++q)
           if (lane + 32 * q < ne) T[(size_t)(lane + 32 * q) * ldT + CB + nf] = rv[q];
       } else {
-        // the accumulators from D_e / r_f (precomputed offsets: no divisions, no branches around the loads)
-        const double* D = a.D + a.offD[l];
-        const double* rf = a.rf + a.offRf[l];
-#pragma unroll
-        for (int s = 0; s < MAXT; ++s) {
-          const int o = offD[s];
-          const double2 v = __ldg(reinterpret_cast<const double2*>(D + (o >= 0 ? o : 0)));
-          const double r0v = __ldg(rf + (o < -1 ? -o - 2 : 0));
-          acc[s][0] = o >= 0 ? v.x : (o < -1 ? r0v : 0.0);
-          acc[s][1] = o >= 0 ? v.y : 0.0;
-        }
+        if (!have_acc) load_acc(l);
+        have_acc = false;
       }
       SW_STAMP(tit, 4);
       if (!GT) mbar_wait(&mbar[0], ph);
@@ -1070,6 +1074,23 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
                                  tid);
         }
       } else {
+        // every worker is past its last read of T / Cr once the last panel's [S | g] update is done: the helper
+        // issues the next element's remaining rows and C rows then, ahead of the [S | g] stores and barrier E
+        // (debug bit 26: after E as before; bit 27: the next D_e / r_f accumulators loaded at the element start).
+        // Measured on C4 in one binary: both 33.6 ms, early loads alone 34.65, early accumulators alone 35.4,
+        // neither 34.05 ms — the element start waits for whichever of the two lands last.
+        const bool eload = !GT && ln >= 0 && !(a.debug & (1 << 26));
+        if (eload) {
+          if (helper) {
+            named_sync(3, (NWK + 1) * 32);
+            if (G.npan == 1) expect_all();
+            fence_proxy_async();
+            load_rows(ln, (G.npan - 1) * NB, ne);
+            load_C(ln);
+          } else {
+            named_arrive(3, (NWK + 1) * 32);
+          }
+        }
         if (helper) {
           int32_t* perm = reinterpret_cast<int32_t*>(LU + (size_t)ne * ne);
           for (int i = lane; i < ne; i += 32) perm[i] = i;
@@ -1099,11 +1120,15 @@ __global__ void __launch_bounds__(NWARPS * 32, MINB) sweep_kernel(const Condense
               else if (o < -1) g[-o - 2] = acc[s][0];
             }
           }
+          if (!GT && ln >= 0 && !(a.debug & (1 << 27))) {   // the next element's accumulators, landing across E
+            load_acc(ln);
+            have_acc = true;
+          }
         }
         SW_STAMP(tit, 6);
         __syncthreads();   // E: every read of T / Cr of this element is done
         SW_STAMP(tit, 7);
-        if (!GT && ln >= 0 && helper) {
+        if (!GT && ln >= 0 && helper && !eload) {
           if (G.npan == 1) expect_all();
           fence_proxy_async();
           load_rows(ln, (G.npan - 1) * NB, ne);

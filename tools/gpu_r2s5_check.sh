@@ -7,3 +7,6 @@ Q="--no-e2e --no-cpu-baseline"
 timeout 300 python bench.py --config C4 --steps 8 --warmup 3 $Q > $O/C4.log 2>&1; show $O/C4.log
 timeout 300 python bench.py --config C5 --slab 0/8 --steps 5 --warmup 3 $Q > $O/C5s.log 2>&1; show $O/C5s.log
 HDG_DEBUG_MODE=256 timeout 300 python bench.py --config C5 --slab 0/8 --steps 5 --warmup 3 $Q > $O/C5s_old.log 2>&1; show $O/C5s_old.log
+for h in 12 13 15 16; do
+  HDG_DEBUG_MODE=$((h << 8)) timeout 300 python bench.py --config C4 --steps 8 --warmup 3 $Q > $O/C4_h$h.log 2>&1; echo "hsel $h"; show $O/C4_h$h.log
+done
