@@ -397,6 +397,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// shared -> global bulk copy (TMA), tracked by the issuing thread's bulk async-groups
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// wait until every committed bulk group of this thread has finished READING its shared-memory source
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 // bulk prefetch of a global range into L2 (TMA engine; no shared memory involved)
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
@@ -520,7 +529,7 @@ constexpr int kBatchK = 16;   // k4-steps of C_e fragments loaded ahead in phase
 template <int NI, int NWARPS>
 __device__ __forceinline__ void schur_items(const SgDst& dst, const double* T, int ldT, int ne, int nf,
                                             int CB, int CTs, int nchunk, const double* Cm, const double* D,
-                                            const double* rf, int warp, int lane) {
+                                            const double* rf, int warp, int lane, bool shareB = false) {
   const int gid = lane >> 2, tig = lane & 3;
   const int nItems = ((nf + 7) >> 3) * nchunk;
   for (int w0 = warp; w0 < nItems; w0 += NI * NWARPS) {
@@ -558,7 +567,20 @@ __device__ __forceinline__ void schur_items(const SgDst& dst, const double* T, i
 #pragma unroll
       for (int q = 0; q < kBatchK; ++q) {
         const int k = k0 + 4 * q;
-        if (k < ne) {
+        if (k < ne && shareB) {
+          // one column chunk (nchunk == 1): the items of a pass share their B fragments — one load per column tile
+          const double* Tk = T + (k + tig) * ldT + CB + gid;
+          double bf[kChunkCT];
+#pragma unroll
+          for (int j = 0; j < kChunkCT; ++j) bf[j] = j < CTs ? Tk[8 * j] : 0.0;
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            const double av = rv[i] ? -cv[i][q] : 0.0;
+#pragma unroll
+            for (int j = 0; j < kChunkCT; ++j)
+              if (j < CTs) dmma(acc[i][j], av, bf[j]);
+          }
+        } else if (k < ne) {
 #pragma unroll
           for (int i = 0; i < NI; ++i) {
             const double av = rv[i] ? -cv[i][q] : 0.0;
@@ -674,10 +696,24 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
       double* LU = reinterpret_cast<double*>(a.factors + a.offF[l]);
       // one warp per row, lanes over column pairs: coalesced 16-byte loads and stores, no index division
       // (ne and ldT are even, so every row start is 16-byte aligned in T and in the record)
-      for (int i = warp; i < ne; i += NWARPS) {
-        const double2* src = reinterpret_cast<const double2*>(T + (size_t)i * ldT);
-        double2* dst = reinterpret_cast<double2*>(LU + (size_t)i * ne);
-        for (int j = lane; j < (ne >> 1); j += 32) dst[j] = src[j];
+      // T in shared memory: the rows leave by TMA bulk stores (shared -> global, one per row, asynchronous: the
+      // backward substitution and [S | g] never touch T's A columns; warp 0 waits for their shared-memory reads
+      // before it streams the next element's A_e in). The warp copy loop cost 5.3 K of C3's 76 K cycles per
+      // element (profiles/r02/trace_panel_C3.txt); debug bit 32 keeps it for the A/B.
+      const bool bulk = T_SMEM && !fail && !(a.debug & 32);
+      if (bulk) {
+        fence_proxy_async();   // every thread's writes of T, ordered before the async-proxy reads
+        __syncthreads();
+        if (warp == 0) {
+          for (int i = lane; i < ne; i += 32) bulk_s2g(LU + (size_t)i * ne, T + (size_t)i * ldT, (uint32_t)ne * 8u);
+          bulk_commit();
+        }
+      } else {
+        for (int i = warp; i < ne; i += NWARPS) {
+          const double2* src = reinterpret_cast<const double2*>(T + (size_t)i * ldT);
+          double2* dst = reinterpret_cast<double2*>(LU + (size_t)i * ne);
+          for (int j = lane; j < (ne >> 1); j += 32) dst[j] = src[j];
+        }
       }
       // row permutation of P A: follow where original row i ends up through the interchanges (parallel in i)
       int32_t* perm = reinterpret_cast<int32_t*>(LU + (int64_t)ne * ne);
@@ -717,6 +753,7 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
     }
     HDG_STAMP(a.trace, tit, 5);
     // the A columns of T are free from here on: start streaming the next element's A_e
+    if (T_SMEM && warp == 0) bulk_wait_read_all();   // the factor rows' bulk stores have read T
     if (T_SMEM && warp == 0 && next < a.count) {
       fence_proxy_async();
       issue_A(elem_of(next));
@@ -730,8 +767,11 @@ __global__ void __launch_bounds__(THREADS, MINB) condense_kernel(const CondenseA
       const double* rf = a.rf + a.offRf[l];
       const int RTs = (nf + 7) >> 3, CTs = (C8 - CB) >> 3;
       const int nchunk = (CTs + kChunkCT - 1) / kChunkCT;
-      if (RTs * nchunk > NWARPS)
-        schur_items<2, NWARPS>(dst, T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, warp, lane);
+      // One item per warp pass (8 accumulator tiles; more passes) measured faster than two (C3 in one binary:
+      // 32.4 vs 33.6 ms; two items sharing their B fragments: 32.8 ms) — debug bit 64 = two items, 128 = shared B
+      if (RTs * nchunk > NWARPS && (a.debug & 64))
+        schur_items<2, NWARPS>(dst, T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, warp, lane,
+                               nchunk == 1 && (a.debug & 128));
       else
         schur_items<1, NWARPS>(dst, T, ldT, ne, nf, CB, CTs, nchunk, Cm, D, rf, warp, lane);
     }

@@ -94,7 +94,8 @@ struct CondenseArgs {
                           // 8 = sweep [S|g] tiles round-robin instead of the row map (A/B); bits 8-13 = the helper warp's
                           // share of the trailing blocks in 64ths (0 = kHelperShare, 1 = the interleaved deal);
                           // bit 26 = the next element's last rows / C rows issued after barrier E, bit 27 = its accumulators
-                          // loaded at its start (the round-2 forms, A/B)
+                          // loaded at its start (the round-2 forms, A/B); panel kernel: 32 = factor rows by a warp copy
+                          // loop instead of TMA bulk stores, 64 = two [S|g] items per warp pass, 128 = with shared B fragments
   // fused condense -> assemble (hdg_condense_assemble, §8(f) NEXT #2): when Kf != NULL, S_e and g_e go straight
   // into K and E by fp64 atomics instead of being stored — every K / E entry has at most two contributions (left
   // and right element of a face) and (0 + a) + b = (0 + b) + a in IEEE arithmetic, so the result is bitwise the
